@@ -1,0 +1,104 @@
+"""ctypes binding of libseesaw_b200.so (the C ABI in include/seesaw_b200.h).
+
+The product path has no fallback: if the library is missing or a call fails,
+:class:`SeesawKernelError` is raised with the library's own error text.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libseesaw_b200.so"
+
+SSB_EPI_NONE = 0
+SSB_EPI_RESIDUAL = 1
+SSB_EPI_SILU_MUL = 2
+SSB_MAX_PEERS = 64
+
+
+class SeesawKernelError(RuntimeError):
+    """A libseesaw_b200 call returned a non-zero status."""
+
+
+class KVGeometry(ctypes.Structure):
+    _fields_ = [
+        ("n_layers", ctypes.c_int),
+        ("n_heads", ctypes.c_int),
+        ("block_size", ctypes.c_int),
+        ("head_dim", ctypes.c_int),
+    ]
+
+
+class CopyDesc(ctypes.Structure):
+    _fields_ = [
+        ("src_off", ctypes.c_int64),
+        ("dst_off", ctypes.c_int64),
+        ("src_stride", ctypes.c_int64),
+        ("dst_stride", ctypes.c_int64),
+        ("cum_bytes", ctypes.c_int64),
+        ("rows", ctypes.c_int32),
+        ("row_bytes", ctypes.c_int32),
+    ]
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_I64 = ctypes.c_int64
+_F = ctypes.c_float
+_PI32 = ctypes.POINTER(ctypes.c_int32)
+_PI64 = ctypes.POINTER(ctypes.c_int64)
+
+# name -> argtypes (restype is int for all compute entry points)
+SIGNATURES: dict[str, list] = {
+    "ssb_gemm_bf16": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P],
+    "ssb_kv_reshard_pack": [_P, KVGeometry, _P, _I, _I, _PI32, _PI32, _PI32, _PI32, _PI64, _P, _P],
+    "ssb_kv_reshard_unpack": [_P, KVGeometry, _P, _I, _I, _PI32, _PI32, _PI32, _PI32, _PI64, _P, _P],
+    "ssb_copy2d_batched": [_P, _P, _P, _I, _I64, _P],
+}
+
+_lock = threading.Lock()
+_lib: ctypes.CDLL | None = None
+
+
+def load() -> ctypes.CDLL:
+    """Load the library once; raise if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise SeesawKernelError(
+                    f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)"
+                )
+            lib = ctypes.CDLL(str(LIB_PATH))
+            lib.ssb_last_error.restype = ctypes.c_char_p
+            lib.ssb_last_error.argtypes = []
+            lib.ssb_version.restype = ctypes.c_int
+            lib.ssb_device_sm_count.restype = ctypes.c_int
+            for name, args in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.argtypes = args
+                fn.restype = ctypes.c_int
+            _lib = lib
+    return _lib
+
+
+def call(name: str, *args) -> None:
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.ssb_last_error().decode(errors="replace")
+        raise SeesawKernelError(f"{name} failed ({rc}): {msg}")
+
+
+def int32_array(values) -> ctypes.Array:
+    vals = list(values)
+    return (ctypes.c_int32 * max(len(vals), 1))(*vals)
+
+
+def int64_array(values) -> ctypes.Array:
+    vals = list(values)
+    return (ctypes.c_int64 * max(len(vals), 1))(*vals)

@@ -1,0 +1,355 @@
+// Persistent, warp-specialised bf16 GEMM on the 5th-generation tensor cores.
+//
+//   C[M, N] = A[M, K] . B[N, K]^T  (+ residual | SiLU(gate) * up)
+//
+// A = activations (row-major, K contiguous), B = a weight matrix stored
+// [out_features, in_features] (K contiguous): both operands are K-major.
+// This kernel replaces the reference's analytic linear-layer terms
+// (perf.py:59-65 weight traffic, perf.py:92-111 linear compute) with the real
+// contraction: QKV / O / gate_up / down projections and the lm_head.
+//
+// Structure (one CTA per SM, 6 warps):
+//   warp 0      TMA producer: A tile 128x64 and B tile BNx64 per k-block into a
+//               STAGES-deep ring of 128B-swizzled shared-memory buffers.
+//   warp 1      allocates TMEM; one lane issues tcgen05.mma (M=128, N=BN,
+//               K=16) into a double-buffered fp32 accumulator in TMEM and
+//               commits completion to mbarriers.
+//   warps 2..5  epilogue: tcgen05.ld 32 lanes x 32 columns, fused epilogue,
+//               bf16 stores.  Accumulator double buffering lets the epilogue
+//               of tile i overlap the MMAs of tile i+1.
+#include "common.cuh"
+#include "seesaw_b200.h"
+
+namespace ssb {
+
+int encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                        uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;       // 64 bf16 = 128 B = one swizzle row
+constexpr int kUmmaK = 16;
+constexpr int kThreads = 192;
+constexpr int kGroupM = 16;   // tile rasterisation: 16 M-tiles share a B band in L2
+
+template <int BN>
+struct Cfg {
+  static constexpr int kStages = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align slack*/ + 256 /*barriers*/;
+};
+
+struct Params {
+  void* C;
+  const void* R;   // residual (may alias C); only for SSB_EPI_RESIDUAL
+  int M, N, K;     // N = columns of the accumulator (gate_up width for SiLU)
+  int ldc, ldr;    // elements
+  int epi;
+  int tiles_m, tiles_n;
+};
+
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& tm, int& tn) {
+  const int per_group = kGroupM * tiles_n;
+  const int group = t / per_group;
+  const int first_m = group * kGroupM;
+  const int gsize = min(tiles_m - first_m, kGroupM);
+  const int local = t - group * per_group;
+  tm = first_m + local % gsize;
+  tn = local / gsize;
+}
+
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmap_a,
+                    const __grid_constant__ CUtensorMap tmap_b, const Params p) {
+  using C = Cfg<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment for the SW128 atoms.
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + C::kStages * C::kABytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + C::kStages;
+  uint64_t* tfull = bars + 2 * C::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_tiles = p.tiles_m * p.tiles_n;
+  const int num_kb = (p.K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmap_a);
+    prefetch_tmap(&tmap_b);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);  // one arrive per epilogue warp
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      const uint64_t pol_a = policy_evict_first();
+      const uint64_t pol_b = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int tm, tn;
+        tile_coords(t, p.tiles_m, p.tiles_n, tm, tn);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+          tma_load_2d(smem_a + stage * C::kABytes, &tmap_a, &full[stage], kb * kBK, tm * kBM,
+                      pol_a);
+          tma_load_2d(smem_b + stage * C::kBBytes, &tmap_b, &full[stage], kb * kBK, tn * BN,
+                      pol_b);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      constexpr uint32_t idesc = idesc_bf16_f32(kBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = sdesc_k_sw128(smem_u32(smem_a + stage * C::kABytes));
+          const uint64_t bdesc = sdesc_k_sw128(smem_u32(smem_b + stage * C::kBBytes));
+#pragma unroll
+          for (int k = 0; k < kBK / kUmmaK; ++k) {
+            // advance 16 elements (32 B) along K inside the 128 B swizzle row
+            umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ---------------- epilogue warps ----------------
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int tm, tn;
+      tile_coords(t, p.tiles_m, p.tiles_n, tm, tn);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = tm * kBM + q * 32 + lane;
+      const bool row_ok = row < p.M;
+      const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+      __nv_bfloat16* crow = reinterpret_cast<__nv_bfloat16*>(p.C) + static_cast<size_t>(row) * p.ldc;
+      if (p.epi == SSB_EPI_SILU_MUL) {
+        // accumulator columns come in (32 gate, 32 up) pairs -> 32 outputs
+#pragma unroll 1
+        for (int c = 0; c < BN / 64; ++c) {
+          uint32_t g[32], u[32];
+          tmem_ld32(tbase + c * 64, g);
+          tmem_ld32(tbase + c * 64 + 32, u);
+          tmem_ld_wait();
+          const int col = (tn * BN) / 2 + c * 32;
+          const int ncols = p.N / 2;
+          if (row_ok) {
+            if (col + 32 <= ncols) {
+              uint4* dst = reinterpret_cast<uint4*>(crow + col);
+#pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                uint4 o;
+                o.x = pack_bf16x2(silu(__uint_as_float(g[8 * v + 0])) * __uint_as_float(u[8 * v + 0]),
+                                  silu(__uint_as_float(g[8 * v + 1])) * __uint_as_float(u[8 * v + 1]));
+                o.y = pack_bf16x2(silu(__uint_as_float(g[8 * v + 2])) * __uint_as_float(u[8 * v + 2]),
+                                  silu(__uint_as_float(g[8 * v + 3])) * __uint_as_float(u[8 * v + 3]));
+                o.z = pack_bf16x2(silu(__uint_as_float(g[8 * v + 4])) * __uint_as_float(u[8 * v + 4]),
+                                  silu(__uint_as_float(g[8 * v + 5])) * __uint_as_float(u[8 * v + 5]));
+                o.w = pack_bf16x2(silu(__uint_as_float(g[8 * v + 6])) * __uint_as_float(u[8 * v + 6]),
+                                  silu(__uint_as_float(g[8 * v + 7])) * __uint_as_float(u[8 * v + 7]));
+                dst[v] = o;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (col + j < ncols)
+                  crow[col + j] = __float2bfloat16_rn(silu(__uint_as_float(g[j])) * __uint_as_float(u[j]));
+            }
+          }
+        }
+      } else {
+        const __nv_bfloat16* rrow =
+            p.epi == SSB_EPI_RESIDUAL
+                ? reinterpret_cast<const __nv_bfloat16*>(p.R) + static_cast<size_t>(row) * p.ldr
+                : nullptr;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t a[32];
+          tmem_ld32(tbase + c * 32, a);
+          tmem_ld_wait();
+          const int col = tn * BN + c * 32;
+          if (row_ok) {
+            float f[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(a[j]);
+            if (col + 32 <= p.N) {
+              if (rrow) {
+                const uint4* src = reinterpret_cast<const uint4*>(rrow + col);
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                  uint4 r = src[v];
+                  f[8 * v + 0] += bf16_lo(r.x); f[8 * v + 1] += bf16_hi(r.x);
+                  f[8 * v + 2] += bf16_lo(r.y); f[8 * v + 3] += bf16_hi(r.y);
+                  f[8 * v + 4] += bf16_lo(r.z); f[8 * v + 5] += bf16_hi(r.z);
+                  f[8 * v + 6] += bf16_lo(r.w); f[8 * v + 7] += bf16_hi(r.w);
+                }
+              }
+              uint4* dst = reinterpret_cast<uint4*>(crow + col);
+#pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                uint4 o;
+                o.x = pack_bf16x2(f[8 * v + 0], f[8 * v + 1]);
+                o.y = pack_bf16x2(f[8 * v + 2], f[8 * v + 3]);
+                o.z = pack_bf16x2(f[8 * v + 4], f[8 * v + 5]);
+                o.w = pack_bf16x2(f[8 * v + 6], f[8 * v + 7]);
+                dst[v] = o;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                if (col + j < p.N) {
+                  float v = f[j];
+                  if (rrow) v += __bfloat162float(rrow[col + j]);
+                  crow[col + j] = __float2bfloat16_rn(v);
+                }
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::kTmemCols);
+  }
+}
+
+template <int BN>
+int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, int K, int lda,
+           int ldb, int ldc, int ldr, int epi, cudaStream_t stream, int max_ctas) {
+  using C = Cfg<BN>;
+  CUtensorMap ta, tb;
+  int rc = encode_tmap_2d_bf16(&ta, A, K, M, static_cast<uint64_t>(lda) * 2, kBK, kBM);
+  if (rc) return rc;
+  rc = encode_tmap_2d_bf16(&tb, B, K, N, static_cast<uint64_t>(ldb) * 2, kBK, BN);
+  if (rc) return rc;
+  static bool attr_done = false;  // per BN instantiation
+  if (!attr_done) {
+    SSB_CUDA(cudaFuncSetAttribute(gemm_bf16_sm100<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  C::kSmemBytes));
+    attr_done = true;
+  }
+  Params p;
+  p.C = Cp;
+  p.R = R;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.ldc = ldc;
+  p.ldr = ldr;
+  p.epi = epi;
+  p.tiles_m = (M + kBM - 1) / kBM;
+  p.tiles_n = (N + BN - 1) / BN;
+  const int tiles = p.tiles_m * p.tiles_n;
+  int grid = num_sms();
+  if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
+  if (tiles < grid) grid = tiles;
+  gemm_bf16_sm100<BN><<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, p);
+  return check_launch("gemm_bf16_sm100");
+}
+
+// Pick the widest N tile that still fills the machine.
+int choose_bn(int M, int N, int sms) {
+  const int tm = (M + kBM - 1) / kBM;
+  const int cands[3] = {256, 128, 64};
+  for (int i = 0; i < 3; ++i) {
+    const int bn = cands[i];
+    const long tiles = static_cast<long>(tm) * ((N + bn - 1) / bn);
+    if (tiles >= sms) return bn;
+  }
+  return 64;
+}
+
+}  // namespace
+}  // namespace ssb
+
+extern "C" int ssb_gemm_bf16(const void* A, const void* B, void* C, const void* R, int M, int N,
+                             int K, int lda, int ldb, int ldc, int ldr, int epilogue, int block_n,
+                             void* stream) {
+  using namespace ssb;
+  SSB_REQUIRE(M > 0 && N > 0 && K > 0, "ssb_gemm_bf16: empty problem M=%d N=%d K=%d", M, N, K);
+  SSB_REQUIRE(A && B && C, "ssb_gemm_bf16: null operand");
+  SSB_REQUIRE(epilogue >= SSB_EPI_NONE && epilogue <= SSB_EPI_SILU_MUL, "ssb_gemm_bf16: bad epilogue %d",
+              epilogue);
+  SSB_REQUIRE(epilogue != SSB_EPI_RESIDUAL || R, "ssb_gemm_bf16: residual epilogue without R");
+  SSB_REQUIRE(lda >= K && ldb >= K, "ssb_gemm_bf16: lda/ldb smaller than K");
+  SSB_REQUIRE(epilogue == SSB_EPI_SILU_MUL ? (N % 64 == 0 && ldc >= N / 2) : ldc >= N,
+              "ssb_gemm_bf16: bad ldc/N for epilogue");
+  if (!aligned16(A) || !aligned16(B) || (lda % 8) || (ldb % 8) || !aligned16(C) || (ldc % 8) ||
+      (R && (!aligned16(R) || (ldr % 8)))) {
+    set_error("ssb_gemm_bf16: operands must be 16-byte aligned with leading dims %% 8 == 0");
+    return SSB_EALIGN;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int bn = block_n;
+  if (bn == 0) bn = choose_bn(M, epilogue == SSB_EPI_SILU_MUL ? N : N, num_sms());
+  switch (bn) {
+    case 256: return launch<256>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, 0);
+    case 128: return launch<128>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, 0);
+    case 64: return launch<64>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, 0);
+    default: return fail_arg("ssb_gemm_bf16: block_n must be 0, 64, 128 or 256 (got %d)", block_n);
+  }
+}

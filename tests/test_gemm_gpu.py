@@ -1,0 +1,75 @@
+"""tcgen05 GEMM vs a plain PyTorch fp32 reference of the same op."""
+
+from __future__ import annotations
+
+import pytest
+import torch
+
+from paper_2503_06433_b200 import ops
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref(a, w):
+    return a.float() @ w.float().T
+
+
+@pytest.mark.parametrize(
+    "M,N,K,bn",
+    [
+        (128, 256, 64, 256),
+        (256, 512, 4096, 256),
+        (1000, 768, 4096, 0),
+        (512, 6144, 4096, 0),
+        (77, 200, 136, 64),
+        (300, 384, 1024, 128),
+        (4096, 4096, 4096, 256),
+    ],
+)
+def test_gemm_plain(cuda, M, N, K, bn):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
+    a = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=cuda, generator=g) / K**0.5).to(torch.bfloat16)
+    out = ops.gemm(a, w, block_n=bn)
+    torch.cuda.synchronize()
+    ref = _ref(a, w)
+    err = (out.float() - ref).abs().max().item()
+    tol = 2e-2 * ref.abs().max().item() + 1e-2
+    assert err <= tol, f"max err {err} > {tol}"
+
+
+def test_gemm_residual_inplace(cuda):
+    M, N, K = 384, 1024, 512
+    a = torch.randn(M, K, device=cuda).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=cuda) / K**0.5).to(torch.bfloat16)
+    r = torch.randn(M, N, device=cuda).to(torch.bfloat16)
+    ref = _ref(a, w) + r.float()
+    ops.gemm(a, w, out=r, residual=r)
+    torch.cuda.synchronize()
+    assert (r.float() - ref).abs().max().item() < 5e-2
+
+
+def test_gemm_silu_mul(cuda):
+    M, F, K = 640, 512, 1024
+    a = torch.randn(M, K, device=cuda).to(torch.bfloat16)
+    gate = (torch.randn(F, K, device=cuda) / K**0.5).to(torch.bfloat16)
+    up = (torch.randn(F, K, device=cuda) / K**0.5).to(torch.bfloat16)
+    # interleave (32 gate, 32 up) row groups
+    w = torch.stack([gate.view(F // 32, 32, K), up.view(F // 32, 32, K)], dim=1).reshape(2 * F, K)
+    out = ops.gemm(a, w, silu_mul=True)
+    torch.cuda.synchronize()
+    g = a.float() @ gate.float().T
+    u = a.float() @ up.float().T
+    ref = torch.nn.functional.silu(g) * u
+    assert (out.float() - ref).abs().max().item() < 3e-2 * ref.abs().max().item() + 1e-2
+
+
+def test_gemm_strided_a(cuda):
+    # A is a column slice of a wider activation (row stride > K)
+    M, K, N = 256, 512, 256
+    big = torch.randn(M, 3 * K, device=cuda).to(torch.bfloat16)
+    a = big[:, K : 2 * K]
+    w = (torch.randn(N, K, device=cuda) / K**0.5).to(torch.bfloat16)
+    out = ops.gemm(a, w)
+    torch.cuda.synchronize()
+    assert (out.float() - _ref(a, w)).abs().max().item() < 5e-2

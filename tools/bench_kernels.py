@@ -1,0 +1,65 @@
+"""Micro-benchmarks of individual kernels (CUDA events, warm-up, L2 flush)."""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2503_06433_b200 import ops  # noqa: E402
+
+L2_FLUSH = torch.empty(0)
+
+
+def timed(fn, iters=20, warmup=3, flush=True):
+    global L2_FLUSH
+    if L2_FLUSH.numel() == 0:
+        L2_FLUSH = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(iters):
+        if flush:
+            L2_FLUSH.zero_()
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        e.synchronize()
+        times.append(s.elapsed_time(e))
+    times.sort()
+    return times[len(times) // 2]
+
+
+def bench_gemm(shapes):
+    out = []
+    for M, N, K, bn in shapes:
+        a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        w = (torch.randn(N, K, device="cuda") / K**0.5).to(torch.bfloat16)
+        c = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        ms = timed(lambda: ops.gemm(a, w, out=c, block_n=bn))
+        ms_t = timed(lambda: torch.matmul(a, w.T, out=c))
+        fl = 2.0 * M * N * K
+        out.append(dict(M=M, N=N, K=K, bn=bn, ms=ms, tflops=fl / ms / 1e9, torch_ms=ms_t,
+                        torch_tflops=fl / ms_t / 1e9))
+        print(json.dumps(out[-1]), flush=True)
+    return out
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--what", default="gemm")
+    args = ap.parse_args()
+    if args.what == "gemm":
+        bench_gemm([
+            (8192, 6144, 4096, 256), (8192, 4096, 4096, 256), (8192, 28672, 4096, 256),
+            (8192, 4096, 14336, 256), (512, 6144, 4096, 0), (512, 4096, 4096, 0),
+            (512, 28672, 4096, 0), (512, 4096, 14336, 0), (512, 128256, 4096, 0),
+            (512, 4096, 4096, 128), (512, 4096, 4096, 64),
+        ])
