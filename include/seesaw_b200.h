@@ -36,6 +36,7 @@ extern "C" {
 #define SSB_EPI_RESIDUAL 1 /* C = A.B^T + R (R may alias C)                   */
 #define SSB_EPI_SILU_MUL 2 /* accumulator columns are (32 gate, 32 up) pairs;
                               C[:, j] = silu(gate_j) * up_j, N/2 columns     */
+#define SSB_EPI_F32 3      /* C = A.B^T stored as fp32 (logits)               */
 
 const char* ssb_last_error(void);
 int ssb_version(void);
@@ -100,6 +101,88 @@ typedef struct ssb_copy_desc {
 /* total_bytes = sum of rows*row_bytes = cum_bytes[n-1] + last size. */
 int ssb_copy2d_batched(const void* src, void* dst, const ssb_copy_desc* descs, int n_desc,
                        int64_t total_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Deterministic weight initialisation (counter-based; see csrc/init.cu).
+ * Not a reference op: it lets every GPU build its own shard of the
+ * random-init model (synthetic weights) bit-identically to the
+ * CPU oracle.  `segs` is a DEVICE array; element (r, c) of segment s is
+ * arena[dst_off + r*ld + c] = value(seed, tensor_id, (row0+r)*full_cols + col0+c).
+ * ---------------------------------------------------------------------- */
+typedef struct ssb_init_seg {
+  int64_t dst_off;   /* elements into the arena                 */
+  int64_t ld;        /* destination row stride (elements)       */
+  int64_t row0;      /* logical origin                          */
+  int64_t col0;
+  int64_t full_cols; /* logical tensor width                    */
+  int64_t cum_elems; /* exclusive prefix of rows*cols           */
+  int32_t rows;
+  int32_t cols;
+  int32_t tensor_id;
+  float scale;       /* std; 0 => constant 1.0 (norm gains)    */
+} ssb_init_seg;
+
+int ssb_init_weights(void* arena, const ssb_init_seg* segs, int n_seg, int64_t total_elems,
+                     uint64_t seed, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Transformer-layer element ops (no reference counterpart: the reference
+ * cost model does not price them).
+ * ---------------------------------------------------------------------- */
+/* out[r,:] = x[i,:] * rsqrt(mean(x[i]^2)+eps) * w with i = row_idx ? row_idx[r] : r
+ * (bf16 in/out, fp32 math; row_idx gathers e.g. the last token of each
+ * prompt before the LM head) */
+int ssb_rmsnorm(const void* x, int ldx, const int32_t* row_idx, const void* w, void* out, int ldo,
+                int rows, int hidden, float eps, void* stream);
+
+/* Decode-step bookkeeping on device: ctx_lens[b] += 1; positions[b] =
+ * ctx_lens[b]-1; slots[b] = block_tables[b][pos/bs]*bs + pos%bs. */
+int ssb_decode_positions(int32_t* ctx_lens, const int32_t* block_tables, int max_blocks,
+                         int block_size, int32_t* positions, int64_t* slots, int batch,
+                         void* stream);
+
+/* In place RoPE (rotate-half) of the q and k heads of qkv[T, (nq+2nk)*d]
+ * (row stride ld) at positions[t] using the fp32 tables cos/sin[max_pos][d/2],
+ * then append k and v of every token to the paged pool at slot
+ * slots[t] = block*block_size + offset, local layer `layer`.  A negative slot
+ * skips the append (padding rows). */
+int ssb_rope_kv_append(void* qkv, int ld, int T, int nq, int nk, const int32_t* positions,
+                       const float* rope_cos, const float* rope_sin, int max_pos, void* pool,
+                       ssb_kv_geometry geo, int layer, const int64_t* slots, void* stream);
+
+/* Vocab-parallel embedding gather: out[t,:] = table[ids[t]-vocab_begin,:]
+ * when the id falls in [vocab_begin, vocab_begin+vocab_local), else zeros. */
+int ssb_embedding(const int32_t* ids, int T, const void* table, int vocab_begin, int vocab_local,
+                  int hidden, void* out, int ldo, void* stream);
+
+/* Per-row argmax of fp32 logits [rows, cols] (row stride ld); ties resolve to
+ * the smallest index; out_idx = index_base + column. */
+int ssb_argmax_rows(const float* logits, int ld, int rows, int cols, int index_base, float* out_val,
+                    int32_t* out_idx, void* stream);
+
+/* Combine n_parts partial argmaxes laid out [n_parts][rows] (vocab-parallel
+ * lm_head): largest value, smallest index on ties. */
+int ssb_argmax_combine(const float* vals, const int32_t* idxs, int n_parts, int rows,
+                       int32_t* out_idx, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Attention.  Replaces perf.py:68-89 / :92-111 (attention traffic and
+ * compute) in _quantum (sim.py:335-341).
+ * ---------------------------------------------------------------------- */
+/* Causal prefill over packed sequences: qkv[T, (nq+2nk)*d] (RoPE applied),
+ * sequence s spans rows [cu_seqlens[s], cu_seqlens[s+1]); out[T, nq*d]. */
+int ssb_prefill_attention(const void* qkv, int ld, int nq, int nk, int head_dim,
+                          const int32_t* cu_seqlens, int nseq, int max_len, void* out, int ldo,
+                          float softmax_scale, void* stream);
+
+/* Paged GQA decode, one query token per sequence: q = qkv[b, 0:nq*d];
+ * K/V of local layer `layer` read from the pool through
+ * block_tables[b][0:ceil(ctx_lens[b]/64)] (block_size must be 64);
+ * out[b, nq*d]. */
+int ssb_decode_attention(const void* qkv, int ld, int nq, int nk, const void* pool,
+                         ssb_kv_geometry geo, int num_blocks, int layer, const int32_t* block_tables,
+                         int max_blocks, const int32_t* ctx_lens, int batch, void* out, int ldo,
+                         float softmax_scale, void* stream);
 
 #ifdef __cplusplus
 }

@@ -15,6 +15,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libseesaw_b200.so"
 SSB_EPI_NONE = 0
 SSB_EPI_RESIDUAL = 1
 SSB_EPI_SILU_MUL = 2
+SSB_EPI_F32 = 3
 SSB_MAX_PEERS = 64
 
 
@@ -56,6 +57,15 @@ SIGNATURES: dict[str, list] = {
     "ssb_kv_reshard_pack": [_P, KVGeometry, _P, _I, _I, _PI32, _PI32, _PI32, _PI32, _PI64, _P, _P],
     "ssb_kv_reshard_unpack": [_P, KVGeometry, _P, _I, _I, _PI32, _PI32, _PI32, _PI32, _PI64, _P, _P],
     "ssb_copy2d_batched": [_P, _P, _P, _I, _I64, _P],
+    "ssb_init_weights": [_P, _P, _I, _I64, ctypes.c_uint64, _P],
+    "ssb_rmsnorm": [_P, _I, _P, _P, _P, _I, _I, _I, _F, _P],
+    "ssb_decode_positions": [_P, _P, _I, _I, _P, _P, _I, _P],
+    "ssb_rope_kv_append": [_P, _I, _I, _I, _I, _P, _P, _P, _I, _P, KVGeometry, _I, _P, _P],
+    "ssb_embedding": [_P, _I, _P, _I, _I, _I, _P, _I, _P],
+    "ssb_argmax_rows": [_P, _I, _I, _I, _I, _P, _P, _P],
+    "ssb_argmax_combine": [_P, _P, _I, _I, _P, _P],
+    "ssb_prefill_attention": [_P, _I, _I, _I, _I, _P, _I, _I, _P, _I, _F, _P],
+    "ssb_decode_attention": [_P, _I, _I, _I, _P, KVGeometry, _I, _I, _P, _I, _P, _I, _P, _I, _F, _P],
 }
 
 _lock = threading.Lock()

@@ -1,0 +1,264 @@
+"""Collective plumbing for the SPMD workers (one process — or thread — per GPU).
+
+The engine only needs five operations over a *group* of ranks: all-to-all
+with uneven splits (weight and KV re-shard), in-place sum all-reduce (TP
+row-parallel outputs), all-gather (vocab-parallel argmax), point-to-point
+send/recv (PP activations) and barrier.
+
+* :class:`TorchComm` — ``torch.distributed`` groups: NCCL over NVLink/NVSwitch
+  on the GPU box (one process per GPU, launched by torchrun), gloo on CPU for
+  the multi-process tests.  NCCL is reached only through torch so exactly one
+  libnccl (torch's bundled 2.28) lives in the process.
+* :class:`ThreadComm` — W virtual ranks as threads of one process sharing one
+  device.  Used to run and test the multi-rank PP→TP path bit-exactly on a
+  single GPU (the only configuration gpurun provides); transfers are device
+  copies between the ranks' buffers, ordered by stream synchronisation.
+"""
+
+from __future__ import annotations
+
+import threading
+from typing import Sequence
+
+import torch
+
+
+class Comm:
+    """Interface: a group of ``size`` ranks; ``rank`` is this member's index."""
+
+    rank: int
+    size: int
+
+    def all_to_all(self, out: torch.Tensor, inp: torch.Tensor, out_splits: Sequence[int],
+                   in_splits: Sequence[int]) -> None:
+        raise NotImplementedError
+
+    def all_reduce_(self, t: torch.Tensor) -> None:
+        raise NotImplementedError
+
+    def all_gather(self, out: torch.Tensor, inp: torch.Tensor) -> None:
+        """out = concat over ranks (dim 0) of inp."""
+        raise NotImplementedError
+
+    def send(self, t: torch.Tensor, dst: int) -> None:
+        raise NotImplementedError
+
+    def recv(self, t: torch.Tensor, src: int) -> None:
+        raise NotImplementedError
+
+    def barrier(self) -> None:
+        raise NotImplementedError
+
+    def subgroup(self, members: Sequence[int]) -> "Comm":
+        """Group of the listed ranks (indices in THIS group); every member of
+        this group must call it with the same lists in the same order."""
+        raise NotImplementedError
+
+
+class SoloComm(Comm):
+    """A group of one."""
+
+    def __init__(self) -> None:
+        self.rank, self.size = 0, 1
+
+    def all_to_all(self, out, inp, out_splits, in_splits) -> None:
+        if out.data_ptr() != inp.data_ptr():
+            out[: int(in_splits[0])].copy_(inp[: int(in_splits[0])])
+
+    def all_reduce_(self, t) -> None:
+        return None
+
+    def all_gather(self, out, inp) -> None:
+        out.view(-1)[: inp.numel()].copy_(inp.reshape(-1))
+
+    def send(self, t, dst) -> None:
+        raise RuntimeError("send in a group of one")
+
+    def recv(self, t, src) -> None:
+        raise RuntimeError("recv in a group of one")
+
+    def barrier(self) -> None:
+        return None
+
+    def subgroup(self, members) -> Comm:
+        return self
+
+
+class TorchComm(Comm):
+    """torch.distributed process group (NCCL on GPU, gloo on CPU)."""
+
+    def __init__(self, group=None, ranks: Sequence[int] | None = None) -> None:
+        import torch.distributed as dist
+
+        self._dist = dist
+        self.group = group
+        self.global_ranks = list(ranks) if ranks is not None else list(range(dist.get_world_size()))
+        self.size = len(self.global_ranks)
+        self.rank = self.global_ranks.index(dist.get_rank())
+
+    def all_to_all(self, out, inp, out_splits, in_splits) -> None:
+        self._dist.all_to_all_single(out, inp, [int(x) for x in out_splits], [int(x) for x in in_splits],
+                                     group=self.group)
+
+    def all_reduce_(self, t) -> None:
+        if self.size > 1:
+            self._dist.all_reduce(t, group=self.group)
+
+    def all_gather(self, out, inp) -> None:
+        self._dist.all_gather_into_tensor(out, inp.contiguous(), group=self.group)
+
+    def send(self, t, dst) -> None:
+        self._dist.send(t, self.global_ranks[dst], group=self.group)
+
+    def recv(self, t, src) -> None:
+        self._dist.recv(t, self.global_ranks[src], group=self.group)
+
+    def barrier(self) -> None:
+        if self.size > 1:
+            self._dist.barrier(group=self.group)
+
+    def subgroup(self, members) -> Comm:
+        ranks = [self.global_ranks[m] for m in members]
+        if len(ranks) == 1:
+            solo = SoloComm()
+            return solo
+        # new_group must be entered by every process of the default group
+        group = _new_group_cached(self._dist, tuple(ranks))
+        return TorchComm(group, ranks) if self._dist.get_rank() in ranks else SoloComm()
+
+
+_GROUPS: dict[tuple[int, ...], object] = {}
+
+
+def _new_group_cached(dist, ranks: tuple[int, ...]):
+    if ranks not in _GROUPS:
+        _GROUPS[ranks] = dist.new_group(list(ranks))
+    return _GROUPS[ranks]
+
+
+class _ThreadWorld:
+    """Shared state of W thread-ranks."""
+
+    def __init__(self, size: int) -> None:
+        self.size = size
+        self.barrier = threading.Barrier(size)
+        self.slots: dict = {}
+        self.lock = threading.Lock()
+        self.mail: dict[tuple[int, int, int], torch.Tensor] = {}
+        self.mail_cv = threading.Condition()
+        self.subworlds: dict[tuple[int, ...], "_ThreadWorld"] = {}
+
+
+class ThreadComm(Comm):
+    """Virtual ranks = threads of one process on one device."""
+
+    def __init__(self, world: _ThreadWorld, rank: int) -> None:
+        self.world = world
+        self.rank = rank
+        self.size = world.size
+        self._seq: dict[tuple[int, int], int] = {}
+
+    @staticmethod
+    def create(size: int) -> list["ThreadComm"]:
+        w = _ThreadWorld(size)
+        return [ThreadComm(w, r) for r in range(size)]
+
+    def _sync(self) -> None:
+        if torch.cuda.is_available():
+            torch.cuda.current_stream().synchronize()
+
+    def _exchange(self, obj):
+        """Publish ``obj`` and return everyone's published objects."""
+        self._sync()
+        w = self.world
+        with w.lock:
+            w.slots[self.rank] = obj
+        w.barrier.wait()
+        objs = [w.slots[r] for r in range(self.size)]
+        return objs
+
+    def _done(self) -> None:
+        self._sync()
+        self.world.barrier.wait()
+
+    def all_to_all(self, out, inp, out_splits, in_splits) -> None:
+        objs = self._exchange((inp, [int(x) for x in in_splits]))
+        src_offs = []
+        for tensor, splits in objs:
+            offs, acc = [], 0
+            for s in splits:
+                offs.append(acc)
+                acc += s
+            src_offs.append(offs)
+        pos = 0
+        for q in range(self.size):
+            n = int(out_splits[q])
+            tensor, splits = objs[q]
+            if splits[self.rank] != n:
+                raise RuntimeError(f"all_to_all split mismatch {splits[self.rank]} != {n}")
+            if n:
+                o = src_offs[q][self.rank]
+                out[pos : pos + n].copy_(tensor[o : o + n])
+            pos += n
+        self._done()
+
+    def all_reduce_(self, t) -> None:
+        if self.size == 1:
+            return
+        objs = self._exchange(t)
+        acc = objs[0].float().clone()
+        for x in objs[1:]:
+            acc += x.float()
+        self._sync()
+        self.world.barrier.wait()  # everyone has read the inputs
+        t.copy_(acc.to(t.dtype))
+        self._done()
+
+    def all_gather(self, out, inp) -> None:
+        objs = self._exchange(inp)
+        n = inp.numel()
+        flat = out.view(-1)
+        for q, x in enumerate(objs):
+            flat[q * n : (q + 1) * n].copy_(x.reshape(-1))
+        self._done()
+
+    def _key(self, src: int, dst: int) -> tuple[int, int, int]:
+        k = (src, dst)
+        self._seq[k] = self._seq.get(k, 0) + 1
+        return (src, dst, self._seq[k])
+
+    def send(self, t, dst) -> None:
+        self._sync()
+        key = self._key(self.rank, dst)
+        w = self.world
+        with w.mail_cv:
+            w.mail[key] = t
+            w.mail_cv.notify_all()
+            # rendezvous: wait until the receiver consumed it (buffer reuse safety)
+            w.mail_cv.wait_for(lambda: key not in w.mail)
+
+    def recv(self, t, src) -> None:
+        key = self._key(src, self.rank)
+        w = self.world
+        with w.mail_cv:
+            w.mail_cv.wait_for(lambda: key in w.mail)
+            t.copy_(w.mail[key])
+            self._sync()
+            del w.mail[key]
+            w.mail_cv.notify_all()
+
+    def barrier(self) -> None:
+        self._done()
+
+    def subgroup(self, members) -> Comm:
+        members = tuple(members)
+        if len(members) == 1:
+            return SoloComm()
+        w = self.world
+        with w.lock:
+            if members not in w.subworlds:
+                w.subworlds[members] = _ThreadWorld(len(members))
+            sub = w.subworlds[members]
+        if self.rank not in members:
+            return SoloComm()
+        return ThreadComm(sub, members.index(self.rank))

@@ -226,7 +226,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             float f[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(a[j]);
-            if (col + 32 <= p.N) {
+            if (p.epi == SSB_EPI_F32) {
+              float* frow = reinterpret_cast<float*>(p.C) + static_cast<size_t>(row) * p.ldc;
+              if (col + 32 <= p.N) {
+                float4* dst = reinterpret_cast<float4*>(frow + col);
+#pragma unroll
+                for (int v = 0; v < 8; ++v)
+                  dst[v] = make_float4(f[4 * v], f[4 * v + 1], f[4 * v + 2], f[4 * v + 3]);
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (col + j < p.N) frow[col + j] = f[j];
+              }
+            } else if (col + 32 <= p.N) {
               if (rrow) {
                 const uint4* src = reinterpret_cast<const uint4*>(rrow + col);
 #pragma unroll
@@ -314,13 +326,9 @@ int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, 
 // Pick the widest N tile that still fills the machine.
 int choose_bn(int M, int N, int sms) {
   const int tm = (M + kBM - 1) / kBM;
-  const int cands[3] = {256, 128, 64};
-  for (int i = 0; i < 3; ++i) {
-    const int bn = cands[i];
-    const long tiles = static_cast<long>(tm) * ((N + bn - 1) / bn);
-    if (tiles >= sms) return bn;
-  }
-  return 64;
+  const long t256 = static_cast<long>(tm) * ((N + 255) / 256);
+  if (t256 >= sms) return 256;
+  return 128;
 }
 
 }  // namespace
@@ -332,13 +340,14 @@ extern "C" int ssb_gemm_bf16(const void* A, const void* B, void* C, const void* 
   using namespace ssb;
   SSB_REQUIRE(M > 0 && N > 0 && K > 0, "ssb_gemm_bf16: empty problem M=%d N=%d K=%d", M, N, K);
   SSB_REQUIRE(A && B && C, "ssb_gemm_bf16: null operand");
-  SSB_REQUIRE(epilogue >= SSB_EPI_NONE && epilogue <= SSB_EPI_SILU_MUL, "ssb_gemm_bf16: bad epilogue %d",
+  SSB_REQUIRE(epilogue >= SSB_EPI_NONE && epilogue <= SSB_EPI_F32, "ssb_gemm_bf16: bad epilogue %d",
               epilogue);
   SSB_REQUIRE(epilogue != SSB_EPI_RESIDUAL || R, "ssb_gemm_bf16: residual epilogue without R");
   SSB_REQUIRE(lda >= K && ldb >= K, "ssb_gemm_bf16: lda/ldb smaller than K");
   SSB_REQUIRE(epilogue == SSB_EPI_SILU_MUL ? (N % 64 == 0 && ldc >= N / 2) : ldc >= N,
               "ssb_gemm_bf16: bad ldc/N for epilogue");
-  if (!aligned16(A) || !aligned16(B) || (lda % 8) || (ldb % 8) || !aligned16(C) || (ldc % 8) ||
+  if (!aligned16(A) || !aligned16(B) || (lda % 8) || (ldb % 8) || !aligned16(C) ||
+      (ldc % (epilogue == SSB_EPI_F32 ? 4 : 8)) ||
       (R && (!aligned16(R) || (ldr % 8)))) {
     set_error("ssb_gemm_bf16: operands must be 16-byte aligned with leading dims %% 8 == 0");
     return SSB_EALIGN;

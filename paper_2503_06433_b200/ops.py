@@ -12,7 +12,7 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import SSB_EPI_NONE, SSB_EPI_RESIDUAL, SSB_EPI_SILU_MUL, call
+from ._lib import SSB_EPI_F32, SSB_EPI_NONE, SSB_EPI_RESIDUAL, SSB_EPI_SILU_MUL, call
 
 
 def _stream() -> int:
@@ -33,8 +33,10 @@ def gemm(
     residual: torch.Tensor | None = None,
     silu_mul: bool = False,
     block_n: int = 0,
+    out_f32: bool = False,
 ) -> torch.Tensor:
-    """out = a @ w.T (+ residual) or silu-mul of interleaved gate/up columns.
+    """out = a @ w.T (+ residual) or silu-mul of interleaved gate/up columns,
+    or fp32 output (logits) with ``out_f32``.
 
     a: [M, K] bf16 (row stride may exceed K), w: [N, K] bf16 weight.
     """
@@ -47,10 +49,14 @@ def gemm(
     if a.stride(1) != 1 or w.stride(1) != 1:
         raise ValueError("gemm: operands must be K-contiguous")
     n_out = N // 2 if silu_mul else N
+    odt = torch.float32 if out_f32 else torch.bfloat16
     if out is None:
-        out = torch.empty((M, n_out), dtype=torch.bfloat16, device=a.device)
-    _check(out, "out")
-    epi = SSB_EPI_SILU_MUL if silu_mul else (SSB_EPI_RESIDUAL if residual is not None else SSB_EPI_NONE)
+        out = torch.empty((M, n_out), dtype=odt, device=a.device)
+    _check(out, "out", odt)
+    if out_f32:
+        epi = SSB_EPI_F32
+    else:
+        epi = SSB_EPI_SILU_MUL if silu_mul else (SSB_EPI_RESIDUAL if residual is not None else SSB_EPI_NONE)
     if residual is not None:
         _check(residual, "residual")
     call(
@@ -128,3 +134,94 @@ def copy2d_batched(src: torch.Tensor, dst: torch.Tensor, descs: torch.Tensor, to
         total_bytes,
         _stream(),
     )
+
+
+def init_weights(arena: torch.Tensor, segs: torch.Tensor, total_elems: int, seed: int) -> None:
+    """Counter-based init of ``arena`` (bf16) from a CUDA int64 [n, 8] segment table."""
+    _check(arena, "arena")
+    if not segs.is_cuda or segs.dtype != torch.int64 or segs.shape[1] != 8:
+        raise ValueError("init_weights: segs must be a CUDA int64 [n, 8] table")
+    call("ssb_init_weights", arena.data_ptr(), segs.data_ptr(), segs.shape[0], total_elems, seed, _stream())
+
+
+def rmsnorm(x: torch.Tensor, w: torch.Tensor, eps: float, out: torch.Tensor | None = None,
+            row_idx: torch.Tensor | None = None) -> torch.Tensor:
+    """RMSNorm of x's rows (or of the rows listed in int32 ``row_idx``)."""
+    _check(x, "x")
+    _check(w, "w")
+    hidden = x.shape[1]
+    rows = row_idx.numel() if row_idx is not None else x.shape[0]
+    if row_idx is not None and row_idx.dtype != torch.int32:
+        raise ValueError("rmsnorm: row_idx must be int32")
+    if out is None:
+        out = torch.empty((rows, hidden), dtype=torch.bfloat16, device=x.device)
+    call("ssb_rmsnorm", x.data_ptr(), x.stride(0), row_idx.data_ptr() if row_idx is not None else None,
+         w.data_ptr(), out.data_ptr(), out.stride(0), rows, hidden, eps, _stream())
+    return out
+
+
+def decode_positions(ctx_lens: torch.Tensor, block_tables: torch.Tensor, block_size: int,
+                     positions: torch.Tensor, slots: torch.Tensor) -> None:
+    """Advance every context by one token and compute its position and pool slot."""
+    call("ssb_decode_positions", ctx_lens.data_ptr(), block_tables.data_ptr(), block_tables.shape[1], block_size,
+         positions.data_ptr(), slots.data_ptr(), ctx_lens.numel(), _stream())
+
+
+def rope_kv_append(qkv: torch.Tensor, nq: int, nk: int, positions: torch.Tensor, rope_cos: torch.Tensor,
+                   rope_sin: torch.Tensor, pool: torch.Tensor | None, geometry, layer: int,
+                   slots: torch.Tensor | None) -> None:
+    """In-place RoPE on q/k heads of ``qkv`` and paged append of k/v (see C ABI)."""
+    _check(qkv, "qkv")
+    if positions.dtype != torch.int32 or rope_cos.dtype != torch.float32:
+        raise ValueError("rope_kv_append: positions int32, tables float32")
+    if slots is not None and slots.dtype != torch.int64:
+        raise ValueError("rope_kv_append: slots must be int64")
+    call("ssb_rope_kv_append", qkv.data_ptr(), qkv.stride(0), qkv.shape[0], nq, nk, positions.data_ptr(),
+         rope_cos.data_ptr(), rope_sin.data_ptr(), rope_cos.shape[0],
+         pool.data_ptr() if pool is not None else None, _lib.KVGeometry(*geometry), layer,
+         slots.data_ptr() if slots is not None else None, _stream())
+
+
+def embedding(ids: torch.Tensor, table: torch.Tensor, vocab_begin: int, out: torch.Tensor) -> torch.Tensor:
+    _check(table, "table")
+    if ids.dtype != torch.int32:
+        raise ValueError("embedding: ids must be int32")
+    call("ssb_embedding", ids.data_ptr(), ids.numel(), table.data_ptr(), vocab_begin, table.shape[0],
+         table.shape[1], out.data_ptr(), out.stride(0), _stream())
+    return out
+
+
+def argmax_rows(logits: torch.Tensor, index_base: int, out_val: torch.Tensor, out_idx: torch.Tensor) -> None:
+    _check(logits, "logits", torch.float32)
+    rows, cols = logits.shape
+    call("ssb_argmax_rows", logits.data_ptr(), logits.stride(0), rows, cols, index_base, out_val.data_ptr(),
+         out_idx.data_ptr(), _stream())
+
+
+def argmax_combine(vals: torch.Tensor, idxs: torch.Tensor, out_idx: torch.Tensor) -> None:
+    parts, rows = vals.shape
+    call("ssb_argmax_combine", vals.data_ptr(), idxs.data_ptr(), parts, rows, out_idx.data_ptr(), _stream())
+
+
+def prefill_attention(qkv: torch.Tensor, nq: int, nk: int, head_dim: int, cu_seqlens: torch.Tensor,
+                      max_len: int, out: torch.Tensor, scale: float) -> torch.Tensor:
+    _check(qkv, "qkv")
+    _check(out, "out")
+    if cu_seqlens.dtype != torch.int32:
+        raise ValueError("prefill_attention: cu_seqlens must be int32")
+    call("ssb_prefill_attention", qkv.data_ptr(), qkv.stride(0), nq, nk, head_dim, cu_seqlens.data_ptr(),
+         cu_seqlens.numel() - 1, max_len, out.data_ptr(), out.stride(0), scale, _stream())
+    return out
+
+
+def decode_attention(qkv: torch.Tensor, nq: int, nk: int, pool: torch.Tensor, geometry, num_blocks: int,
+                     layer: int, block_tables: torch.Tensor, ctx_lens: torch.Tensor, out: torch.Tensor,
+                     scale: float) -> torch.Tensor:
+    _check(qkv, "qkv")
+    _check(out, "out")
+    if block_tables.dtype != torch.int32 or ctx_lens.dtype != torch.int32:
+        raise ValueError("decode_attention: block tables and context lengths must be int32")
+    call("ssb_decode_attention", qkv.data_ptr(), qkv.stride(0), nq, nk, pool.data_ptr(),
+         _lib.KVGeometry(*geometry), num_blocks, layer, block_tables.data_ptr(), block_tables.shape[1],
+         ctx_lens.data_ptr(), ctx_lens.numel(), out.data_ptr(), out.stride(0), scale, _stream())
+    return out

@@ -1,0 +1,381 @@
+"""Per-GPU worker: owns one GPU's weights, paged KV pool and buffers, and runs
+the prefill (PP layout) and decode (TP layout) forwards and the re-shard.
+
+One Worker per rank (process or thread); all ranks run the same SPMD program
+and make identical decisions, so no control messages are exchanged — only
+data moves (NCCL / ThreadComm).  Every FLOP and every byte of layout
+transformation is done by libseesaw_b200.so kernels (ops.py); torch provides
+allocation and streams.
+
+What replaces what in the reference (paths under shardsim/):
+  prefill micro-batch quantum  sim.py:360-432 / perf.py  -> :meth:`prefill`
+  transition weight reload     sim.py:328-333, reshard.py:125-148 -> :meth:`repartition_weights`
+  KV re-shard via host tier    sim.py:382, reshard.py:170-188      -> :meth:`reshard_kv`
+  decode quantum               sim.py:517-565 / perf.py  -> :meth:`decode_step`
+"""
+
+from __future__ import annotations
+
+import math
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import ops
+from .arch import LlamaArch
+from .comm import Comm
+from .layout import KVPoolGeometry, WeightLayout, kv_geometry, logical_tensors, repartition_pieces, weight_layout
+from .reshard import kv_exchange
+from .specs import ModelSpec, ParallelismConfig
+
+
+def rope_tables(arch: LlamaArch, max_pos: int) -> tuple[np.ndarray, np.ndarray]:
+    """cos/sin [max_pos, d/2] fp32, computed in float64 on the host so the CPU
+    oracle and the GPU use bit-identical tables (rotate-half RoPE)."""
+    d = arch.head_dim
+    inv = arch.rope_theta ** (-np.arange(0, d, 2, dtype=np.float64) / d)
+    ang = np.arange(max_pos, dtype=np.float64)[:, None] * inv[None, :]
+    return np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32)
+
+
+def init_segment_table(layout: WeightLayout) -> tuple[np.ndarray, int]:
+    """int64 [n, 8] rows of ssb_init_seg for every segment of the layout."""
+    logical = logical_tensors(layout.arch)
+    rows = []
+    cum = 0
+    for t in layout.tensors.values():
+        for s in t.segments:
+            lg = logical[s.logical]
+            scale_bits = struct.unpack("<i", struct.pack("<f", np.float32(lg.scale)))[0]
+            rows.append([
+                t.offset + s.dst_row * t.cols + s.dst_col, t.cols, s.row0, s.col0, lg.cols, cum,
+                (s.rows & 0xFFFFFFFF) | (s.cols << 32),
+                (lg.tensor_id & 0xFFFFFFFF) | ((scale_bits & 0xFFFFFFFF) << 32),
+            ])
+            cum += s.rows * s.cols
+    arr = np.array(rows, dtype=np.uint64).astype(np.int64) if rows else np.zeros((0, 8), np.int64)
+    return arr, cum
+
+
+def _copy_desc_rows(entries: list[tuple[int, int, int, int, int, int]]) -> tuple[np.ndarray, int]:
+    """(src_off, dst_off, src_stride, dst_stride, rows, row_bytes) -> int64 [n, 6] with prefix."""
+    out = np.zeros((len(entries), 6), dtype=np.int64)
+    cum = 0
+    for i, (so, do, ss, ds, rows, rb) in enumerate(entries):
+        out[i] = (so, do, ss, ds, cum, (rows & 0xFFFFFFFF) | (rb << 32))
+        cum += rows * rb
+    return out, cum
+
+
+@dataclass
+class LayoutState:
+    cfg: ParallelismConfig
+    gpu: int                 # index inside the replica
+    stage: int
+    rank: int                # tensor rank
+    weights: WeightLayout
+    arena: torch.Tensor
+    tp_comm: Comm
+    pp_prev: int | None      # replica-group index of the previous stage peer
+    pp_next: int | None
+
+
+class Worker:
+    """One GPU of the fleet (SPMD)."""
+
+    def __init__(self, arch: LlamaArch, world: Comm, dp: int, device: torch.device, seed: int = 0,
+                 block_size: int = 64, max_pos: int = 4096) -> None:
+        self.arch = arch
+        self.world = world
+        self.device = device
+        self.seed = seed
+        self.block_size = block_size
+        self.dp = dp
+        self.per_replica = world.size // dp
+        self.replica, self.gpu = divmod(world.rank, self.per_replica)
+        self.replica_comm = world.subgroup([self.replica * self.per_replica + i for i in range(self.per_replica)])
+        cos, sin = rope_tables(arch, max_pos)
+        self.rope_cos = torch.from_numpy(cos).to(device)
+        self.rope_sin = torch.from_numpy(sin).to(device)
+        self.state: LayoutState | None = None
+        self.pool: torch.Tensor | None = None
+        self.num_blocks = 0
+        self.scale = 1.0 / math.sqrt(arch.head_dim)
+        self._comm_cache: dict = {}
+        self.stream = torch.cuda.current_stream(device) if device.type == "cuda" else None
+        self.record_logits = False
+        self.logit_log: list[torch.Tensor] = []
+        self.stats: dict[str, float] = {}
+        # test/inspection callbacks invoked by the engine: name -> fn(worker, **kw)
+        self.hooks: dict = {}
+
+    # ------------------------------------------------------------ layouts --
+    def _tp_comm(self, cfg: ParallelismConfig, stage: int) -> Comm:
+        key = ("tp", cfg.tp, cfg.pp)
+        if key not in self._comm_cache:
+            # every rank of the replica creates every stage's group (same order)
+            groups = [self.replica_comm.subgroup([s * cfg.tp + r for r in range(cfg.tp)]) for s in range(cfg.pp)]
+            self._comm_cache[key] = groups
+        return self._comm_cache[key][stage]
+
+    def make_layout(self, cfg: ParallelismConfig, arena: torch.Tensor | None = None) -> LayoutState:
+        stage, rank = divmod(self.gpu, cfg.tp)
+        wl = weight_layout(self.arch, cfg.tp, cfg.pp, self.gpu)
+        if arena is None:
+            arena = torch.empty(wl.arena_elems, dtype=torch.bfloat16, device=self.device)
+        prev_ = (stage - 1) * cfg.tp + rank if stage > 0 else None
+        next_ = (stage + 1) * cfg.tp + rank if stage < cfg.pp - 1 else None
+        return LayoutState(cfg, self.gpu, stage, rank, wl, arena, self._tp_comm(cfg, stage), prev_, next_)
+
+    def init_weights(self, cfg: ParallelismConfig) -> None:
+        """Generate this GPU's shard of the random-init model under ``cfg``."""
+        st = self.make_layout(cfg)
+        table, total = init_segment_table(st.weights)
+        segs = torch.from_numpy(table).to(self.device)
+        ops.init_weights(st.arena, segs, total, self.seed)
+        self.state = st
+
+    def w(self, key: str) -> torch.Tensor:
+        t = self.state.weights.tensors[key]
+        return self.state.arena[t.offset : t.offset + t.numel].view(t.rows, t.cols)
+
+    def has(self, key: str) -> bool:
+        return key in self.state.weights.tensors
+
+    # --------------------------------------------------------------- pool --
+    def geometry(self, cfg: ParallelismConfig | None = None) -> KVPoolGeometry:
+        cfg = cfg or self.state.cfg
+        return kv_geometry(self.arch, cfg.tp, cfg.pp, self.num_blocks, self.block_size)
+
+    def alloc_pool(self, num_blocks: int) -> None:
+        """One allocation serves every layout: a block has the same byte size
+        under any (tp, pp) with the same tp*pp."""
+        self.num_blocks = num_blocks
+        geo = self.geometry()
+        self.pool = torch.empty(num_blocks * geo.block_elems, dtype=torch.bfloat16, device=self.device)
+
+    # ------------------------------------------------------- re-partition --
+    def repartition_weights(self, cfg_new: ParallelismConfig) -> int:
+        """Weight column/row re-partition over the replica group; returns bytes
+        this GPU sent to other GPUs."""
+        old = self.state
+        new = self.make_layout(cfg_new)
+        n = self.per_replica
+        old_layouts = [weight_layout(self.arch, old.cfg.tp, old.cfg.pp, g) for g in range(n)]
+        new_layouts = [weight_layout(self.arch, cfg_new.tp, cfg_new.pp, g) for g in range(n)]
+        send_entries, recv_entries = [], []
+        send_splits, recv_splits = [], []
+        s_pos = r_pos = 0
+        for q in range(n):
+            pieces = repartition_pieces(old_layouts[self.gpu], new_layouts[q])
+            start = s_pos
+            for p in pieces:
+                send_entries.append((p.src_off * 2, s_pos * 2, p.src_ld * 2, p.cols * 2, p.rows, p.cols * 2))
+                s_pos += p.numel
+            send_splits.append(s_pos - start)
+            pieces = repartition_pieces(old_layouts[q], new_layouts[self.gpu])
+            start = r_pos
+            for p in pieces:
+                recv_entries.append((r_pos * 2, p.dst_off * 2, p.cols * 2, p.dst_ld * 2, p.rows, p.cols * 2))
+                r_pos += p.numel
+            recv_splits.append(r_pos - start)
+        send = torch.empty(max(s_pos, 8), dtype=torch.bfloat16, device=self.device)
+        recv = torch.empty(max(r_pos, 8), dtype=torch.bfloat16, device=self.device)
+        sd, stot = _copy_desc_rows(send_entries)
+        rd, rtot = _copy_desc_rows(recv_entries)
+        if stot:
+            ops.copy2d_batched(old.arena, send, torch.from_numpy(sd).to(self.device), stot)
+        self.replica_comm.all_to_all(recv, send, recv_splits, send_splits)
+        if rtot:
+            ops.copy2d_batched(recv, new.arena, torch.from_numpy(rd).to(self.device), rtot)
+        self.state = new
+        return 2 * (s_pos - send_splits[self.gpu])
+
+    # ---------------------------------------------------------- KV reshard --
+    def reshard_kv(self, cfg_new: ParallelismConfig, block_ids: np.ndarray, chunk_blocks: int = 256) -> int:
+        """In-place KV re-layout of the listed pool blocks from the current
+        layout to ``cfg_new`` (pack -> all-to-all -> unpack per chunk).
+        Returns the bytes this GPU sent to other GPUs."""
+        model = self.arch.model_spec()
+        src_cfg = ParallelismConfig(self.state.cfg.tp, self.state.cfg.pp, 1)
+        dst_cfg = ParallelismConfig(cfg_new.tp, cfg_new.pp, 1)
+        ex = kv_exchange(model, src_cfg, dst_cfg, self.gpu)
+        geo_s = kv_geometry(self.arch, src_cfg.tp, src_cfg.pp, self.num_blocks, self.block_size)
+        geo_d = kv_geometry(self.arch, dst_cfg.tp, dst_cfg.pp, self.num_blocks, self.block_size)
+        cell = 2 * self.block_size * self.arch.head_dim  # elements of one (layer, head) per block
+        sent = 0
+        ids_all = np.asarray(block_ids, dtype=np.int32)
+        if ids_all.size == 0:
+            return 0
+        max_cells_s = sum(r.cells for r in ex.send)
+        max_cells_r = sum(r.cells for r in ex.recv)
+        chunk = min(chunk_blocks, ids_all.size)
+        send = torch.empty(chunk * max_cells_s * cell + 8, dtype=torch.bfloat16, device=self.device)
+        recv = torch.empty(chunk * max_cells_r * cell + 8, dtype=torch.bfloat16, device=self.device)
+        for c0 in range(0, ids_all.size, chunk):
+            ids_np = ids_all[c0 : c0 + chunk]
+            nid = ids_np.size
+            ids = torch.from_numpy(ids_np).to(self.device)
+            s_peers, r_peers, s_splits, r_splits = [], [], [], []
+            so = ro = 0
+            for q in range(self.per_replica):
+                rs, rr = ex.send[q], ex.recv[q]
+                s_peers.append((rs.l0, rs.nl, rs.h0, rs.nh, so * 2))
+                r_peers.append((rr.l0, rr.nl, rr.h0, rr.nh, ro * 2))
+                s_splits.append(nid * rs.cells * cell)
+                r_splits.append(nid * rr.cells * cell)
+                so += s_splits[-1]
+                ro += r_splits[-1]
+            ops.kv_reshard_pack(self.pool, geo_s.as_tuple(), ids, s_peers, send)
+            self.replica_comm.all_to_all(recv, send, r_splits, s_splits)
+            ops.kv_reshard_unpack(self.pool, geo_d.as_tuple(), ids, r_peers, recv)
+            sent += 2 * (so - s_splits[self.gpu])
+        return sent
+
+    # ------------------------------------------------------------- forward --
+    def _layers(self) -> range:
+        wl = self.state.weights
+        return range(wl.layer_begin, wl.layer_end)
+
+    def _block(self, x: torch.Tensor, layer: int, attn_fn, buf: dict) -> None:
+        """One transformer layer on x (in place); attn_fn(qkv, layer_local) -> attn out."""
+        st = self.state
+        eps = self.arch.rms_eps
+        p = f"L{layer}."
+        lead = st.rank == 0
+        h = ops.rmsnorm(x, self.w(p + "attn_norm"), eps, out=buf["h"])
+        qkv = ops.gemm(h, self.w(p + "wqkv"), out=buf["qkv"])
+        attn = attn_fn(qkv, layer - st.weights.layer_begin)
+        ops.gemm(attn, self.w(p + "wo"), out=x, residual=x if lead else None)
+        self._reduce_into(x)
+        h = ops.rmsnorm(x, self.w(p + "mlp_norm"), eps, out=buf["h"])
+        act = ops.gemm(h, self.w(p + "w13"), out=buf["act"], silu_mul=True)
+        ops.gemm(act, self.w(p + "w2"), out=x, residual=x if lead else None)
+        self._reduce_into(x)
+
+    def _reduce_into(self, x: torch.Tensor) -> None:
+        """Row-parallel combine: rank 0 added the residual in its GEMM epilogue,
+        the others hold partial sums; the all-reduce yields residual + sum."""
+        if self.state.tp_comm.size > 1:
+            self.state.tp_comm.all_reduce_(x)
+
+    def _buffers(self, T: int) -> dict:
+        st = self.state
+        a = self.arch
+        nq, nk = st.weights.n_q_heads, st.weights.n_kv_heads
+        key = ("buf", T, st.cfg.tp)
+        if self._comm_cache.get("buf_key") != key:
+            dev = self.device
+            self._comm_cache["buf"] = {
+                "h": torch.empty(T, a.hidden, dtype=torch.bfloat16, device=dev),
+                "qkv": torch.empty(T, (nq + 2 * nk) * a.head_dim, dtype=torch.bfloat16, device=dev),
+                "attn": torch.empty(T, nq * a.head_dim, dtype=torch.bfloat16, device=dev),
+                "act": torch.empty(T, st.weights.ffn_local, dtype=torch.bfloat16, device=dev),
+            }
+            self._comm_cache["buf_key"] = key
+        return self._comm_cache["buf"]
+
+    def _logits_argmax(self, h_last: torch.Tensor, out_tokens: torch.Tensor) -> None:
+        """Vocab-parallel LM head + greedy argmax (fp32 logits)."""
+        st = self.state
+        n = h_last.shape[0]
+        logits = ops.gemm(h_last, self.w("head"), out_f32=True)
+        vals = torch.empty(n, dtype=torch.float32, device=self.device)
+        idxs = torch.empty(n, dtype=torch.int32, device=self.device)
+        ops.argmax_rows(logits, st.weights.vocab_begin, vals, idxs)
+        if self.record_logits:
+            self._record(logits)
+        if st.tp_comm.size == 1:
+            out_tokens.copy_(idxs)
+            return
+        P = st.tp_comm.size
+        gv = torch.empty(P * n, dtype=torch.float32, device=self.device)
+        gi = torch.empty(P * n, dtype=torch.int32, device=self.device)
+        st.tp_comm.all_gather(gv, vals)
+        st.tp_comm.all_gather(gi, idxs)
+        ops.argmax_combine(gv.view(P, n), gi.view(P, n), out_tokens)
+
+    def _record(self, logits: torch.Tensor) -> None:
+        st = self.state
+        if st.tp_comm.size > 1:
+            P = st.tp_comm.size
+            g = torch.empty(P * logits.numel(), dtype=torch.float32, device=self.device)
+            st.tp_comm.all_gather(g, logits.contiguous())
+            logits = g.view(P, *logits.shape).permute(1, 0, 2).reshape(logits.shape[0], -1)
+        self.logit_log.append(logits.detach().float().cpu())
+
+    def prefill(self, tokens: torch.Tensor, cu_seqlens: np.ndarray, tables: np.ndarray,
+                first_tokens: torch.Tensor) -> None:
+        """Prefill a micro-batch of packed prompts through this GPU's stage.
+
+        tokens: int32 [T] on device (used on stage 0); cu_seqlens: host
+        int32 [n+1]; tables: host int32 [n, max_blocks].  Stage s>0 receives
+        the activations from s-1, stage s<pp-1 sends to s+1; the last stage
+        writes the greedy first token of every prompt into first_tokens[n]."""
+        st = self.state
+        a = self.arch
+        T = int(cu_seqlens[-1])
+        n = len(cu_seqlens) - 1
+        buf = self._buffers(T)
+        x = torch.empty(T, a.hidden, dtype=torch.bfloat16, device=self.device)
+        if st.stage == 0:
+            ops.embedding(tokens, self.w("embed"), st.weights.vocab_begin, x)
+            if st.tp_comm.size > 1:
+                st.tp_comm.all_reduce_(x)
+        else:
+            self.replica_comm.recv(x, st.pp_prev)
+        pos = np.concatenate([np.arange(cu_seqlens[i + 1] - cu_seqlens[i], dtype=np.int32) for i in range(n)])
+        seq_of = np.repeat(np.arange(n), np.diff(cu_seqlens))
+        bs = self.block_size
+        slots = tables[seq_of, pos // bs].astype(np.int64) * bs + pos % bs
+        pos_d = torch.from_numpy(pos).to(self.device)
+        slots_d = torch.from_numpy(slots).to(self.device)
+        cu_d = torch.from_numpy(np.asarray(cu_seqlens, dtype=np.int32)).to(self.device)
+        max_len = int(np.max(np.diff(cu_seqlens)))
+        geo = self.geometry()
+        nq, nk = st.weights.n_q_heads, st.weights.n_kv_heads
+
+        def attn(qkv, layer_local):
+            ops.rope_kv_append(qkv, nq, nk, pos_d, self.rope_cos, self.rope_sin, self.pool, geo.as_tuple(),
+                               layer_local, slots_d)
+            return ops.prefill_attention(qkv, nq, nk, a.head_dim, cu_d, max_len, buf["attn"], self.scale)
+
+        for layer in self._layers():
+            self._block(x, layer, attn, buf)
+        if st.stage < st.cfg.pp - 1:
+            self.replica_comm.send(x, st.pp_next)
+            return
+        last = torch.from_numpy(np.asarray(cu_seqlens[1:], dtype=np.int32) - 1).to(self.device)
+        h_last = ops.rmsnorm(x, self.w("final_norm"), a.rms_eps, row_idx=last)
+        self._logits_argmax(h_last, first_tokens)
+
+    def decode_step(self, tokens: torch.Tensor, ctx_lens: torch.Tensor, tables: torch.Tensor,
+                    positions: torch.Tensor, slots: torch.Tensor, out_tokens: torch.Tensor) -> None:
+        """One decode step of the resident batch under a pure-TP layout:
+        tokens[B] in, next greedy tokens into out_tokens[B]; ctx_lens grows by one."""
+        st = self.state
+        a = self.arch
+        B = tokens.numel()
+        buf = self._buffers(B)
+        x = buf.setdefault("x", torch.empty(B, a.hidden, dtype=torch.bfloat16, device=self.device))
+        if x.shape[0] != B:
+            x = buf["x"] = torch.empty(B, a.hidden, dtype=torch.bfloat16, device=self.device)
+        ops.decode_positions(ctx_lens, tables, self.block_size, positions, slots)
+        ops.embedding(tokens, self.w("embed"), st.weights.vocab_begin, x)
+        if st.tp_comm.size > 1:
+            st.tp_comm.all_reduce_(x)
+        geo = self.geometry()
+        nq, nk = st.weights.n_q_heads, st.weights.n_kv_heads
+
+        def attn(qkv, layer_local):
+            ops.rope_kv_append(qkv, nq, nk, positions, self.rope_cos, self.rope_sin, self.pool, geo.as_tuple(),
+                               layer_local, slots)
+            return ops.decode_attention(qkv, nq, nk, self.pool, geo.as_tuple(), self.num_blocks, layer_local,
+                                        tables, ctx_lens, buf["attn"], self.scale)
+
+        for layer in self._layers():
+            self._block(x, layer, attn, buf)
+        h = ops.rmsnorm(x, self.w("final_norm"), a.rms_eps, out=buf["h"])
+        self._logits_argmax(h, out_tokens)

@@ -1,0 +1,175 @@
+"""End-to-end PP-prefill → re-shard → TP-decode on the tiny config
+(BASELINE.json configs[0]: 2 layers, hidden 256, 4 heads, 8 prompts x 64/32,
+PP=2 -> TP=2) on ONE GPU with two virtual ranks (ThreadComm threads).
+
+Checks, against the CPU oracle:
+  * the run's event log passes replay_check and has the reference's shape;
+  * re-sharded weights are bit-exact with the oracle's shards;
+  * the re-sharded KV pool is bit-exact with the oracle's re-layout of the
+    pre-transition pool;
+  * greedy token ids are identical to the bf16-faithful oracle;
+  * logits are within bf16 tolerance of the fp32 oracle (teacher forced).
+"""
+
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import kv_layout as kvo
+from oracle import llama as lo
+from paper_2503_06433_b200 import PRESETS, execute, replay_check
+from paper_2503_06433_b200.comm import ThreadComm
+from paper_2503_06433_b200.engine import synthetic_prompts
+from paper_2503_06433_b200.layout import logical_tensors
+from paper_2503_06433_b200.report import SchedulingPolicy
+from paper_2503_06433_b200.runtime import Worker
+from paper_2503_06433_b200.specs import HardwareSpec, ParallelismConfig, Request, RingAllReduce
+
+pytestmark = pytest.mark.gpu
+
+
+def tiny_hw(n: int) -> HardwareSpec:
+    return HardwareSpec(num_gpus=n, hbm_bandwidth=8e12, peak_flops=2.25e15, gpu_memory=2e9,
+                        host_memory_per_gpu=2e9, host_link_bandwidth=64e9, allreduce=RingAllReduce(9e11))
+
+
+def oracle_arch(a) -> lo.Arch:
+    return lo.Arch(a.num_layers, a.hidden, a.num_query_heads, a.num_kv_heads, a.head_dim, a.ffn, a.vocab,
+                   a.rope_theta, a.rms_eps)
+
+
+def run_threads(n, fn):
+    out, errs = [None] * n, []
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            out[r] = fn(r)
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+            raise
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(n)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    if errs:
+        raise errs[0]
+    return out
+
+
+def _run_tiny(arch_name: str, cfg_p, cfg_d, n_req=8, s_in=64, s_out=32):
+    arch = PRESETS[arch_name]
+    model = arch.model_spec()
+    W = cfg_p.num_gpus
+    hw = tiny_hw(W)
+    reqs = [Request(i, s_in, s_out) for i in range(n_req)]
+    prompts = synthetic_prompts(reqs, arch.vocab)
+    comms = ThreadComm.create(W)
+    snaps = {}
+
+    def body(r):
+        dev = torch.device("cuda", 0)
+        wk = Worker(arch, comms[r], cfg_p.dp, dev, seed=0, max_pos=256)
+
+        def before(w, blocks, cfg_to):
+            snaps[(r, "pool_before", cfg_to)] = (w.pool.detach().cpu().clone(), blocks.copy(), w.state.cfg)
+
+        def after(w, blocks, cfg_to):
+            snaps[(r, "pool_after", cfg_to)] = w.pool.detach().cpu().clone()
+            snaps[(r, "arena_after", cfg_to)] = (w.state.arena.detach().cpu().clone(), w.state.weights)
+
+        wk.hooks = {"before_reshard": before, "after_reshard": after}
+        rep = execute(model, hw, reqs, SchedulingPolicy.TRANSITION_MINIMIZING, cfg_p, cfg_d, arch=arch,
+                      prompts=prompts, comm=comms[r], device=dev, worker=wk, record_logits=True)
+        return rep, wk
+
+    res = run_threads(W, body)
+    return arch, reqs, prompts, res, snaps
+
+
+@pytest.fixture(scope="module")
+def tiny_run(cuda):
+    return _run_tiny("tiny", ParallelismConfig(1, 2, 1), ParallelismConfig(2, 1, 1))
+
+
+def test_event_log_and_replay(tiny_run):
+    arch, reqs, prompts, res, _ = tiny_run
+    rep = res[0][0]
+    assert replay_check(rep), replay_check(rep).violation
+    kinds = {}
+    for e in rep.event_log:
+        kinds[e.kind] = kinds.get(e.kind, 0) + 1
+    assert rep.transitions == 1
+    assert kinds["prefill_complete"] == 8 and kinds["kv_release"] == 8
+    assert kinds["decode_step"] == 32 and kinds["phase_start"] == 2 and kinds["transition"] == 1
+    assert rep.tokens_per_second > 0
+    assert abs(rep.prefill_time + rep.decode_time + rep.reshard_time + rep.stalled_transfer_time
+               - rep.makespan) <= 1e-6 * max(rep.makespan, 1.0)
+
+
+def test_weights_bit_exact_after_repartition(tiny_run):
+    arch, _, _, _, snaps = tiny_run
+    oa = oracle_arch(arch)
+    specs = lo.tensor_specs(oa)
+    logical = logical_tensors(arch)
+    for r in range(2):
+        arena, wl = snaps[(r, "arena_after", ParallelismConfig(2, 1, 1))]
+        arena = arena.float().numpy()
+        for t in wl.tensors.values():
+            local = arena[t.offset : t.offset + t.numel].reshape(t.rows, t.cols)
+            for s in t.segments:
+                full = lo.init_tensor(0, specs[s.logical])
+                assert logical[s.logical].tensor_id == specs[s.logical][0]
+                exp = full[s.row0 : s.row0 + s.rows, s.col0 : s.col0 + s.cols]
+                got = local[s.dst_row : s.dst_row + s.rows, s.dst_col : s.dst_col + s.cols]
+                np.testing.assert_array_equal(got, exp, err_msg=f"rank {r} {t.key} {s.logical}")
+
+
+def test_kv_pool_bit_exact_after_reshard(tiny_run):
+    arch, _, _, _, snaps = tiny_run
+    cfg_d = ParallelismConfig(2, 1, 1)
+    before = [snaps[(r, "pool_before", cfg_d)] for r in range(2)]
+    blocks = before[0][1]
+    L, H, D, BS = arch.num_layers, arch.num_kv_heads, arch.head_dim, 64
+    src = before[0][2]
+    pools = [b[0].view(torch.int16).numpy().reshape(-1, L // src.pp, 2, H // src.tp, BS, D) for b in before]
+    expect = kvo.reshard_pools(pools, L, H, (src.tp, src.pp), (cfg_d.tp, cfg_d.pp), blocks=blocks)
+    for r in range(2):
+        got = snaps[(r, "pool_after", cfg_d)].view(torch.int16).numpy().reshape(expect[r].shape)
+        np.testing.assert_array_equal(got[blocks], expect[r][blocks])
+
+
+def test_greedy_tokens_match_oracle(tiny_run):
+    arch, reqs, prompts, res, _ = tiny_run
+    rep = res[0][0]
+    oracle = lo.LlamaOracle(oracle_arch(arch), seed=0, bf16_faithful=True, max_pos=256)
+    mism = []
+    for r, p in zip(reqs, prompts):
+        exp, _ = oracle.generate(p, r.output_len)
+        got = rep.outputs[r.id]
+        if got != exp:
+            mism.append((r.id, got, exp))
+    assert not mism, f"{len(mism)} sequences differ; first: {mism[0]}"
+
+
+def test_logits_within_bf16_tolerance(tiny_run):
+    arch, reqs, prompts, res, _ = tiny_run
+    rep, wk = res[1]  # rank 1 = last PP stage: holds the prefill logits too
+    oracle = lo.LlamaOracle(oracle_arch(arch), seed=0, bf16_faithful=False, max_pos=256)
+    logs = wk.logit_log
+    n = len(reqs)
+    prefill = torch.cat(logs[:n])            # one micro-batch per sequence at pp=2
+    decode = logs[n:]                         # [B, V] per step
+    for i, (r, p) in enumerate(zip(reqs, prompts)):
+        toks = rep.outputs[r.id]
+        _, ref = oracle.generate(p, r.output_len, forced=toks)
+        got = [prefill[i]] + [decode[k][i] for k in range(r.output_len - 1)]
+        for k, (g, e) in enumerate(zip(got, ref)):
+            err = (g - e).abs().max().item()
+            assert err <= 0.05 * e.abs().max().item() + 0.02, f"seq {r.id} step {k}: max err {err}"

@@ -1,0 +1,52 @@
+"""The C-ABI library loads without a GPU and exports every symbol the public
+header declares; argument errors come back as negative codes with a message
+(no GPU work is issued by these calls)."""
+
+from __future__ import annotations
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_2503_06433_b200 import _lib
+
+HEADER = Path(__file__).resolve().parent.parent / "include" / "seesaw_b200.h"
+
+
+def declared_functions() -> list[str]:
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(ssb_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_entry_points():
+    names = declared_functions()
+    assert "ssb_gemm_bf16" in names and "ssb_kv_reshard_pack" in names and len(names) >= 15
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, f"missing exports: {missing}"
+    assert lib.ssb_version() == 1
+
+
+def test_ctypes_signatures_cover_header():
+    declared = set(declared_functions())
+    bound = set(_lib.SIGNATURES) | {"ssb_last_error", "ssb_version", "ssb_device_sm_count"}
+    assert declared == bound
+
+
+def test_argument_errors_are_reported_not_raised():
+    lib = _lib.load()
+    rc = lib.ssb_gemm_bf16(None, None, None, None, 0, 0, 0, 0, 0, 0, 0, 0, 0, None)
+    assert rc < 0
+    assert b"empty problem" in lib.ssb_last_error()
+    with pytest.raises(_lib.SeesawKernelError, match="n_peers"):
+        geo = _lib.KVGeometry(1, 1, 64, 128)
+        arr = _lib.int32_array([0])
+        p32 = ctypes.cast(arr, ctypes.POINTER(ctypes.c_int32))
+        p64 = ctypes.cast(_lib.int64_array([0]), ctypes.POINTER(ctypes.c_int64))
+        _lib.call("ssb_kv_reshard_pack", None, geo, None, 1, 0, p32, p32, p32, p32, p64, None, None)
