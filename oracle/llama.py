@@ -126,14 +126,24 @@ def rope_tables(a: Arch, max_pos: int) -> tuple[torch.Tensor, torch.Tensor]:
 
 
 class LlamaOracle:
-    """Greedy generation with a per-sequence KV cache (fp32 or bf16-faithful)."""
+    """Greedy generation with a per-sequence KV cache (fp32 or bf16-faithful).
+
+    In bf16-faithful mode the oracle also reproduces the GPU's *structure*
+    where it changes rounding: tensor-parallel partial sums are rounded to
+    bf16 per rank before the all-reduce (rank 0 adds the residual in its GEMM
+    epilogue), and attention runs the kernels' online softmax — 64-key tiles
+    in prefill, per-warp 16-key slices of 64-token pool blocks in decode —
+    with bf16 probabilities entering the PV product.  ``tp_prefill`` /
+    ``tp_decode`` are the tensor-parallel degrees of the two phases."""
 
     def __init__(self, a: Arch, seed: int, bf16_faithful: bool = True, max_pos: int = 4096,
-                 weights: dict[str, torch.Tensor] | None = None) -> None:
+                 weights: dict[str, torch.Tensor] | None = None, tp_prefill: int = 1, tp_decode: int = 1) -> None:
         self.a = a
         self.bf = bf16_faithful
         self.W = weights if weights is not None else init_model(a, seed)
         self.cos, self.sin = rope_tables(a, max_pos)
+        self.tp_prefill, self.tp_decode = tp_prefill, tp_decode
+        self.tp = tp_prefill
 
     def _r(self, x: torch.Tensor) -> torch.Tensor:
         return x.to(torch.bfloat16).to(torch.float32) if self.bf else x
@@ -166,23 +176,74 @@ class LlamaOracle:
         g = hq // hk
         Kx = K.repeat_interleave(g, dim=1)  # [S, hq, d]
         Vx = V.repeat_interleave(g, dim=1)
-        s = torch.einsum("thd,shd->hts", q, Kx) / math.sqrt(d)
-        S = K.shape[0]
-        qpos = pos[:, None]
-        kpos = torch.arange(S)[None, :]
-        s = s.masked_fill((kpos > qpos)[None], float("-inf"))
-        m = s.amax(-1, keepdim=True)
-        e = torch.exp(s - m)
-        l_ = e.sum(-1, keepdim=True)
-        pe = self._r(e)  # the GPU feeds bf16 probabilities to the PV product
-        o = torch.einsum("hts,shd->thd", pe, Vx) / l_.permute(1, 0, 2)
+        if self.bf:
+            o = self._attn_tiled(q, Kx, Vx, pos)
+        else:
+            s = torch.einsum("thd,shd->hts", q, Kx) / math.sqrt(d)
+            S = K.shape[0]
+            s = s.masked_fill((torch.arange(S)[None, :] > pos[:, None])[None], float("-inf"))
+            o = torch.einsum("hts,shd->thd", torch.softmax(s, -1), Vx)
         o = self._r(o.reshape(-1, hq * d))
-        x = self._r(x + o @ W[p + "wo"].T)
+        x = self._row_parallel(x, o, W[p + "wo"])
         h = self._norm(x, W[p + "mlp_norm"])
         gte = h @ W[p + "w1"].T
         up = h @ W[p + "w3"].T
         act = self._r(torch.nn.functional.silu(gte) * up)
-        return self._r(x + act @ W[p + "w2"].T)
+        return self._row_parallel(x, act, W[p + "w2"])
+
+    def _row_parallel(self, x: torch.Tensor, a: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+        """x + a @ w^T; with tp > 1 in bf16 mode, rank r's partial over its
+        column slice is rounded to bf16 (rank 0 including x) and the partials
+        are summed in fp32 in rank order, then rounded — the GPU's
+        GEMM-epilogue residual + all-reduce."""
+        if not self.bf or self.tp == 1:
+            return self._r(x + a @ w.T)
+        k = a.shape[1] // self.tp
+        acc = None
+        for r in range(self.tp):
+            part = a[:, r * k : (r + 1) * k] @ w[:, r * k : (r + 1) * k].T
+            part = self._r(part + x) if r == 0 else self._r(part)
+            acc = part if acc is None else acc + part
+        return self._r(acc)
+
+    def _attn_tiled(self, q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, pos: torch.Tensor) -> torch.Tensor:
+        """Online softmax in exp2 domain with the kernels' key partitioning."""
+        S = K.shape[0]
+        decode = q.shape[0] == 1 and S > 1 and pos[0].item() == S - 1 and getattr(self, "_decoding", False)
+        if decode:
+            # 4 warps; warp w owns keys 64j + 16w .. +16 of every 64-key block
+            parts = []
+            for w_ in range(4):
+                idx = torch.cat([torch.arange(j + 16 * w_, max(min(j + 16 * w_ + 16, S), j + 16 * w_))
+                                 for j in range(0, S, 64)])
+                parts.append(idx)
+            states = [self._online(q, K, V, pos, [pi]) for pi in parts if pi.numel()]
+            M = torch.stack([m for m, _, _ in states]).amax(0)
+            Mu = torch.where(torch.isinf(M), torch.zeros_like(M), M)
+            L = sum(l_ * torch.exp2(m - Mu) for m, l_, _ in states)
+            O = sum(o * torch.exp2(m - Mu)[..., None] for m, _, o in states)
+            return (O / L[..., None]).permute(1, 0, 2)
+        tiles = [torch.arange(j, min(j + 64, S)) for j in range(0, S, 64)]
+        m, l_, o = self._online(q, K, V, pos, tiles)
+        return (o / l_[..., None]).permute(1, 0, 2)
+
+    def _online(self, q, K, V, pos, chunks):
+        c = torch.tensor(1.0 / math.sqrt(self.a.head_dim) * 1.4426950408889634, dtype=torch.float32)
+        H, T, d = q.shape[1], q.shape[0], q.shape[2]
+        m = torch.full((H, T), float("-inf"))
+        l_ = torch.zeros(H, T)
+        o = torch.zeros(H, T, d)
+        for idx in chunks:
+            s = torch.einsum("thd,shd->hts", q, K[idx]) * c
+            s = s.masked_fill((idx[None, :] > pos[:, None])[None], float("-inf"))
+            m_new = torch.maximum(m, s.amax(-1))
+            mu = torch.where(torch.isinf(m_new), torch.zeros_like(m_new), m_new)
+            corr = torch.exp2(m - mu)
+            pexp = torch.exp2(s - mu[..., None])
+            l_ = l_ * corr + pexp.sum(-1)
+            o = o * corr[..., None] + torch.einsum("hts,shd->htd", self._r(pexp), V[idx])
+            m = m_new
+        return m, l_, o
 
     def _forward(self, ids: torch.Tensor, pos: torch.Tensor, cache) -> torch.Tensor:
         x = self.W["embed"][ids.long()]
@@ -200,9 +261,11 @@ class LlamaOracle:
         cache: dict = {}
         ids = torch.from_numpy(np.asarray(prompt, dtype=np.int64))
         pos = torch.arange(ids.numel())
+        self.tp, self._decoding = self.tp_prefill, False
         logits = self._forward(ids, pos, cache)
         out, logs = [int(torch.argmax(logits))], [logits]
         n = ids.numel()
+        self.tp, self._decoding = self.tp_decode, True
         for k in range(1, output_len):
             tok = forced[k - 1] if forced is not None else out[-1]
             logits = self._forward(torch.tensor([tok]), torch.tensor([n + k - 1]), cache)

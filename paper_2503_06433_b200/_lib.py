@@ -96,9 +96,36 @@ def load() -> ctypes.CDLL:
     return _lib
 
 
+class LaunchStats:
+    """Counts library launches; optionally brackets each with CUDA events
+    (bench.py's per-kernel timing inside the timed region)."""
+
+    def __init__(self) -> None:
+        self.count = 0
+        self.timing = False
+        self.records: list = []   # (tag, start_event, end_event, flops, bytes)
+        self.tagger = None        # fn(name, args) -> (tag, flops, bytes)
+
+
+STATS = LaunchStats()
+
+
 def call(name: str, *args) -> None:
     lib = load()
-    rc = getattr(lib, name)(*args)
+    st = STATS
+    st.count += 1
+    if st.timing:
+        import torch
+
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        rc = getattr(lib, name)(*args)
+        e.record()
+        tag = st.tagger(name, args) if st.tagger else (name, 0, 0)
+        st.records.append((tag[0], s, e, tag[1], tag[2]))
+    else:
+        rc = getattr(lib, name)(*args)
     if rc != 0:
         msg = lib.ssb_last_error().decode(errors="replace")
         raise SeesawKernelError(f"{name} failed ({rc}): {msg}")

@@ -199,9 +199,14 @@ class _Engine:
             if policy is SchedulingPolicy.TRANSITION_MINIMIZING and k > self.cpu_capacity:
                 raise SimulationError(f"request {req.id!r} needs {k} KV bytes but the CPU tier holds "
                                       f"{self.cpu_capacity:.0f}; it can never be buffered")
-            pr = np.asarray(pr, dtype=np.int32)
-            if pr.size != req.input_len:
-                raise SimulationError(f"request {req.id!r}: prompt has {pr.size} ids, input_len {req.input_len}")
+            if isinstance(pr, torch.Tensor):
+                if pr.dtype != torch.int32:
+                    pr = pr.to(torch.int32)
+            else:
+                pr = np.asarray(pr, dtype=np.int32)
+            n_ids = pr.numel() if isinstance(pr, torch.Tensor) else pr.size
+            if n_ids != req.input_len:
+                raise SimulationError(f"request {req.id!r}: prompt has {n_ids} ids, input_len {req.input_len}")
             self.seqs.append(_Seq(req=req, replica=i % self.dp, kv_bytes=k, prompt=pr))
         if len(prompts) != len(requests):
             raise SimulationError("prompts and workload differ in length")
@@ -236,8 +241,12 @@ class _Engine:
     # ---------------------------------------------------------------- run --
     def run(self) -> SimReport:
         w = self.worker
-        if w.state is None or w.state.cfg != self.cfg_p:
+        if w.state is None:
             w.init_weights(self.cfg_p)
+        elif w.state.cfg != self.cfg_p:
+            # weights still in a previous run's decode layout: move them back
+            # over NVLink (the reference starts every run in cfg_p, uncharged)
+            w.repartition_weights(self.cfg_p)
         if w.pool is None or w.num_blocks < self.num_blocks:
             w.alloc_pool(self.num_blocks)
         self.alloc = BlockAllocator(w.num_blocks)
@@ -336,7 +345,11 @@ class _Engine:
             tables = np.zeros((len(mb), self.max_blocks), dtype=np.int32)
             for i, s in enumerate(mb):
                 tables[i, : len(s.blocks)] = s.blocks
-            toks = torch.from_numpy(np.concatenate([s.prompt for s in mb])).to(self.device)
+            if isinstance(mb[0].prompt, torch.Tensor):
+                # device-resident or pinned-host prompt ids
+                toks = torch.cat([s.prompt for s in mb]).to(self.device, non_blocking=True)
+            else:
+                toks = torch.from_numpy(np.concatenate([s.prompt for s in mb])).to(self.device)
             w.prefill(toks, cu, tables, first[pos : pos + len(mb)])
             pos += len(mb)
         # every rank of the replica needs the first tokens: only the last

