@@ -298,11 +298,16 @@ def profile_kernels(one, prompts, arch, args, dev, comm, world) -> dict:
 
 
 # ------------------------------------------------------- CPU baseline --
-def cpu_baseline(args, arch, sample_in: int = 256, sample_out: int = 2) -> dict:
-    """The CPU restatement (oracle, fp32 torch, all host threads) on a bounded
-    sample: one prompt of ``sample_in`` tokens through the full model, then
-    ``sample_out`` decode steps; extrapolated to the workload's tokens/s as
-    output_len / (T_prefill(input_len) + output_len * T_decode)."""
+_CPU_WEIGHTS: dict = {}
+
+
+def cpu_baseline(args, arch, sample_in: int = 256, batch: int = 8) -> dict:
+    """The CPU restatement (oracle/llama.py, fp32 torch, all host threads) on
+    a bounded sample of the workload: one prompt of ``sample_in`` tokens
+    through the full model (prefill cost per token), then one decode step of
+    ``batch`` new tokens (the GEMM shapes of a batch-``batch`` decode step).
+    Extrapolated to the whole batch: T = P*S_in*t_tok + S_out*(P/batch)*t_step,
+    value = P*S_out / T (GEMM-dominated, linear in tokens)."""
     import torch
 
     from oracle import llama as lo
@@ -311,8 +316,10 @@ def cpu_baseline(args, arch, sample_in: int = 256, sample_out: int = 2) -> dict:
     torch.set_num_threads(threads)
     oa = lo.Arch(arch.num_layers, arch.hidden, arch.num_query_heads, arch.num_kv_heads, arch.head_dim, arch.ffn,
                  arch.vocab, arch.rope_theta, arch.rms_eps)
-    weights = _cpu_weights(arch)
-    orc = lo.LlamaOracle(oa, seed=0, bf16_faithful=False, max_pos=sample_in + sample_out + 8, weights=weights)
+    if arch.name not in _CPU_WEIGHTS:
+        _CPU_WEIGHTS[arch.name] = _cpu_weights(arch)
+    orc = lo.LlamaOracle(oa, seed=0, bf16_faithful=False, max_pos=sample_in + batch + 8,
+                         weights=_CPU_WEIGHTS[arch.name])
     prompt = np.random.default_rng(1).integers(0, arch.vocab, size=sample_in).astype(np.int64)
     cache: dict = {}
     t0 = time.perf_counter()
@@ -320,19 +327,17 @@ def cpu_baseline(args, arch, sample_in: int = 256, sample_out: int = 2) -> dict:
     logits = orc._forward(torch.from_numpy(prompt), torch.arange(sample_in), cache)
     t1 = time.perf_counter()
     tok = int(torch.argmax(logits))
-    orc._decoding = True
-    for k in range(sample_out):
-        logits = orc._forward(torch.tensor([tok]), torch.tensor([sample_in + k]), cache)
-        tok = int(torch.argmax(logits))
+    orc._forward(torch.full((batch,), tok), torch.arange(sample_in, sample_in + batch), cache)
     t2 = time.perf_counter()
-    t_pre = (t1 - t0) * (args.input_len / sample_in)  # linear-in-tokens extrapolation (GEMM-dominated)
-    t_dec = (t2 - t1) / sample_out
-    per_seq = t_pre + args.output_len * t_dec
-    return {"value": args.output_len / per_seq, "unit": "tokens/s", "cores": threads, "kind": "port",
-            "sample": f"1 prompt x {sample_in} in / {sample_out} out through all {arch.num_layers} layers of "
-                      f"{arch.name} (oracle/llama.py fp32, bf16 weights); prefill scaled x{args.input_len / sample_in:g} "
-                      f"to {args.input_len} tokens, {args.output_len} decode steps at the measured step time",
-            "measured_prefill_s": t1 - t0, "measured_decode_step_s": t_dec}
+    t_tok = (t1 - t0) / sample_in
+    t_step = t2 - t1
+    P, S_in, S_out = args.prompts, args.input_len, args.output_len
+    total = P * S_in * t_tok + S_out * (P / batch) * t_step
+    return {"value": P * S_out / total, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"1 prompt x {sample_in} tokens prefilled + one {batch}-token decode step through all "
+                      f"{arch.num_layers} layers of {arch.name} (oracle/llama.py fp32 on bf16 weights); "
+                      f"extrapolated to {P} x {S_in}/{S_out} as P*S_in*t_tok + S_out*(P/{batch})*t_step",
+            "measured_prefill_s": t1 - t0, "measured_decode_step_s": t_step}
 
 
 def _cpu_weights(arch):

@@ -97,8 +97,9 @@ class TorchComm(Comm):
         self.rank = self.global_ranks.index(dist.get_rank())
 
     def all_to_all(self, out, inp, out_splits, in_splits) -> None:
-        self._dist.all_to_all_single(out, inp, [int(x) for x in out_splits], [int(x) for x in in_splits],
-                                     group=self.group)
+        os_, is_ = [int(x) for x in out_splits], [int(x) for x in in_splits]
+        # staging buffers are allocated for the largest chunk: pass exact views
+        self._dist.all_to_all_single(out[: sum(os_)], inp[: sum(is_)], os_, is_, group=self.group)
 
     def all_reduce_(self, t) -> None:
         if self.size > 1:

@@ -50,16 +50,24 @@ struct Params {
   int ldc, ldr;    // elements
   int epi;
   int tiles_m, tiles_n;
+  int group_n;     // rasterisation band orientation (see tile_coords)
 };
 
-__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& tm, int& tn) {
-  const int per_group = kGroupM * tiles_n;
+// Grouped rasterisation: kGroupM tiles of the "band" dimension share one
+// operand band in L2 while the other operand streams.  group_n = 0 bands along
+// M (A band resident, B streamed once per band); group_n = 1 bands along N.
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int group_n, int& tm, int& tn) {
+  const int band_tiles = group_n ? tiles_n : tiles_m;
+  const int other_tiles = group_n ? tiles_m : tiles_n;
+  const int per_group = kGroupM * other_tiles;
   const int group = t / per_group;
-  const int first_m = group * kGroupM;
-  const int gsize = min(tiles_m - first_m, kGroupM);
+  const int first = group * kGroupM;
+  const int gsize = min(band_tiles - first, kGroupM);
   const int local = t - group * per_group;
-  tm = first_m + local % gsize;
-  tn = local / gsize;
+  const int b = first + local % gsize;
+  const int o = local / gsize;
+  tm = group_n ? o : b;
+  tn = group_n ? b : o;
 }
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
@@ -109,13 +117,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
-      const uint64_t pol_a = policy_evict_first();
-      const uint64_t pol_b = policy_evict_last();
+      // the banded operand is re-read by every tile of its band: keep it in
+      // L2; the streamed operand is read by the band's tiles in one wave
+      const uint64_t pol_a = p.group_n ? policy_evict_first() : policy_evict_last();
+      const uint64_t pol_b = p.group_n ? policy_evict_last() : policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         int tm, tn;
-        tile_coords(t, p.tiles_m, p.tiles_n, tm, tn);
+        tile_coords(t, p.tiles_m, p.tiles_n, p.group_n, tm, tn);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
@@ -170,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       int tm, tn;
-      tile_coords(t, p.tiles_m, p.tiles_n, tm, tn);
+      tile_coords(t, p.tiles_m, p.tiles_n, p.group_n, tm, tn);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = tm * kBM + q * 32 + lane;
@@ -315,6 +325,14 @@ int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, 
   p.epi = epi;
   p.tiles_m = (M + kBM - 1) / kBM;
   p.tiles_n = (N + BN - 1) / BN;
+  // band the operand whose re-streaming would cost more DRAM traffic:
+  // M-bands re-read B once per band, N-bands re-read A once per band
+  {
+    const double a_bytes = 2.0 * M * K, b_bytes = 2.0 * N * K;
+    const double m_band = a_bytes + b_bytes * ((p.tiles_m + kGroupM - 1) / kGroupM);
+    const double n_band = b_bytes + a_bytes * ((p.tiles_n + kGroupM - 1) / kGroupM);
+    p.group_n = n_band < m_band ? 1 : 0;
+  }
   const int tiles = p.tiles_m * p.tiles_n;
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
