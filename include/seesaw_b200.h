@@ -103,6 +103,28 @@ int ssb_copy2d_batched(const void* src, void* dst, const ssb_copy_desc* descs, i
                        int64_t total_bytes, void* stream);
 
 /* ------------------------------------------------------------------------
+ * Host KV tier staging (swap-out gather K3 / swap-in scatter K4).
+ * Replaces the swap transfer charges of the reference: swap-out
+ * sum(kv)/out_bw overlapped with prefill (sim.py:382-385) and the prefetcher's
+ * swap-in at in_bw (sim.py:436-504), in the HND host layout
+ * (reshard.py:191-201).
+ * One sequence's KV in this GPU's pool (blocks[0:n_blocks], n_tokens tokens)
+ * <-> contiguous HND staging [nl][2][nh][n_tokens][head_dim] covering pool
+ * layers [l0, l0+nl) and heads [h0, h0+nh).  gather=1: pool -> staging,
+ * gather=0: staging -> pool.  The caller moves staging <-> pinned host memory
+ * with cudaMemcpyAsync on its copy stream. */
+int ssb_kv_hnd_copy(int gather, void* pool, ssb_kv_geometry geo, const int32_t* blocks,
+                    int n_blocks, int n_tokens, int l0, int nl, int h0, int nh, void* staging,
+                    void* stream);
+
+/* Strided host<->device copy (cudaMemcpy2DAsync, direction inferred from
+ * the pointers; host memory must be pinned/registered for asynchrony):
+ * `height` rows of `width` bytes.  Moves a GPU's (layer x head) rectangle
+ * of a sequence between the staging buffer and the shared host-tier slot. */
+int ssb_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
+                       int64_t height, void* stream);
+
+/* ------------------------------------------------------------------------
  * Deterministic weight initialisation (counter-based; see csrc/init.cu).
  * Not a reference op: it lets every GPU build its own shard of the
  * random-init model (synthetic weights) bit-identically to the

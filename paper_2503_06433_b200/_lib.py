@@ -58,6 +58,8 @@ SIGNATURES: dict[str, list] = {
     "ssb_kv_reshard_unpack": [_P, KVGeometry, _P, _I, _I, _PI32, _PI32, _PI32, _PI32, _PI64, _P, _P],
     "ssb_copy2d_batched": [_P, _P, _P, _I, _I64, _P],
     "ssb_init_weights": [_P, _P, _I, _I64, ctypes.c_uint64, _P],
+    "ssb_kv_hnd_copy": [_I, _P, KVGeometry, _P, _I, _I, _I, _I, _I, _I, _P, _P],
+    "ssb_memcpy2d_async": [_P, _I64, _P, _I64, _I64, _I64, _P],
     "ssb_rmsnorm": [_P, _I, _P, _P, _P, _I, _I, _I, _F, _P],
     "ssb_decode_positions": [_P, _P, _I, _I, _P, _P, _I, _P],
     "ssb_rope_kv_append": [_P, _I, _I, _I, _I, _P, _P, _P, _I, _P, KVGeometry, _I, _P, _P],

@@ -54,6 +54,15 @@ class Comm:
         this group must call it with the same lists in the same order."""
         raise NotImplementedError
 
+    def share_host_buffer(self, nbytes: int) -> torch.Tensor:
+        """A pinned host buffer visible to every member of the group (the
+        shared host KV tier).  Collective."""
+        raise NotImplementedError
+
+
+def _pinned(nbytes: int) -> torch.Tensor:
+    return torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=torch.cuda.is_available())
+
 
 class SoloComm(Comm):
     """A group of one."""
@@ -82,6 +91,9 @@ class SoloComm(Comm):
 
     def subgroup(self, members) -> Comm:
         return self
+
+    def share_host_buffer(self, nbytes: int) -> torch.Tensor:
+        return _pinned(nbytes)
 
 
 class TorchComm(Comm):
@@ -127,8 +139,31 @@ class TorchComm(Comm):
         group = _new_group_cached(self._dist, tuple(ranks))
         return TorchComm(group, ranks) if self._dist.get_rank() in ranks else SoloComm()
 
+    def share_host_buffer(self, nbytes: int) -> torch.Tensor:
+        """POSIX shared memory created by the group's first rank, mapped and
+        cudaHostRegister'ed by every process: one host KV tier per replica
+        without the two-stage GPU->pinned->shared copy of PAPER.md:133."""
+        from multiprocessing import shared_memory
+
+        name = [None]
+        if self.rank == 0:
+            shm = shared_memory.SharedMemory(create=True, size=max(nbytes, 1))
+            name = [shm.name]
+        self._dist.broadcast_object_list(name, src=self.global_ranks[0], group=self.group)
+        if self.rank != 0:
+            shm = shared_memory.SharedMemory(name=name[0])
+        buf = torch.frombuffer(shm.buf, dtype=torch.uint8, count=max(nbytes, 1))
+        if torch.cuda.is_available():
+            rc = torch.cuda.cudart().cudaHostRegister(buf.data_ptr(), buf.numel(), 1)  # portable
+            if int(rc) != 0:
+                raise RuntimeError(f"cudaHostRegister of the shared host tier failed ({rc})")
+        _SHM_KEEPALIVE.append(shm)
+        self.barrier()
+        return buf
+
 
 _GROUPS: dict[tuple[int, ...], object] = {}
+_SHM_KEEPALIVE: list = []
 
 
 def _new_group_cached(dist, ranks: tuple[int, ...]):
@@ -250,6 +285,12 @@ class ThreadComm(Comm):
 
     def barrier(self) -> None:
         self._done()
+
+    def share_host_buffer(self, nbytes: int) -> torch.Tensor:
+        objs = self._exchange(_pinned(nbytes) if self.rank == 0 else None)
+        buf = objs[0]
+        self._done()
+        return buf
 
     def subgroup(self, members) -> Comm:
         members = tuple(members)

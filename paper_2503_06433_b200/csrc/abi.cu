@@ -86,4 +86,17 @@ int ssb_version(void) { return SSB_ABI_VERSION; }
 
 int ssb_device_sm_count(void) { return ssb::num_sms(); }
 
+int ssb_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
+                       int64_t height, void* stream) {
+  using namespace ssb;
+  SSB_REQUIRE(width >= 0 && height >= 0 && dpitch >= width && spitch >= width,
+              "ssb_memcpy2d_async: bad geometry");
+  if (width == 0 || height == 0) return 0;
+  SSB_REQUIRE(dst && src, "ssb_memcpy2d_async: null pointer");
+  SSB_CUDA(cudaMemcpy2DAsync(dst, static_cast<size_t>(dpitch), src, static_cast<size_t>(spitch),
+                             static_cast<size_t>(width), static_cast<size_t>(height), cudaMemcpyDefault,
+                             reinterpret_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
 }  // extern "C"

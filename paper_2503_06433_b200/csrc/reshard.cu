@@ -160,10 +160,71 @@ __global__ void __launch_bounds__(kCopyThreads)
   }
 }
 
+// ------------------------------------------------ host-tier gather/scatter --
+// One sequence's KV between the paged pool and the contiguous HND staging
+// layout [layer][K|V][head][token][dim] of the host tier (reshard.py:191-201,
+// PAPER.md:151-154).  The staging covers pool layers [l0, l0+nl) and heads
+// [h0, h0+nh) of this GPU, i.e. this GPU's (layer x head) rectangle of the
+// sequence in its CURRENT layout.  CTA = one (layer, kv, head, block) run of
+// min(64, tokens left) x dim elements.
+template <bool kGather>
+__global__ void __launch_bounds__(kCopyThreads) kv_hnd_kernel(
+    uint8_t* __restrict__ pool, uint8_t* __restrict__ stage, const int32_t* __restrict__ blocks, int n_blocks,
+    int n_tokens, ssb_kv_geometry geo, int l0, int nl, int h0, int nh) {
+  const int run = blockIdx.x;
+  const int b = run % n_blocks;
+  int rest = run / n_blocks;
+  const int h = rest % nh;
+  rest /= nh;
+  const int kv = rest & 1;
+  const int l = rest >> 1;
+  const int64_t row_bytes = static_cast<int64_t>(geo.head_dim) * 2;
+  const int tok0 = b * geo.block_size;
+  const int ntok = min(geo.block_size, n_tokens - tok0);
+  if (ntok <= 0) return;
+  const int64_t blk = blocks[b];
+  const int64_t pool_off =
+      (((blk * geo.n_layers + (l0 + l)) * 2 + kv) * geo.n_heads + (h0 + h)) * geo.block_size * row_bytes;
+  const int64_t stage_off = (((static_cast<int64_t>(l) * 2 + kv) * nh + h) * n_tokens + tok0) * row_bytes;
+  const int64_t n16 = (ntok * row_bytes) >> 4;
+  if (kGather)
+    cta_copy(reinterpret_cast<const uint4*>(pool + pool_off), reinterpret_cast<uint4*>(stage + stage_off), n16);
+  else
+    cta_copy(reinterpret_cast<const uint4*>(stage + stage_off), reinterpret_cast<uint4*>(pool + pool_off), n16);
+}
+
 }  // namespace
 }  // namespace ssb
 
 extern "C" {
+
+int ssb_kv_hnd_copy(int gather, void* pool, ssb_kv_geometry geo, const int32_t* blocks, int n_blocks,
+                    int n_tokens, int l0, int nl, int h0, int nh, void* staging, void* stream) {
+  using namespace ssb;
+  SSB_REQUIRE(n_blocks >= 0 && n_tokens >= 0 && nl >= 0 && nh >= 0, "ssb_kv_hnd_copy: negative sizes");
+  if (n_blocks == 0 || n_tokens == 0 || nl == 0 || nh == 0) return 0;
+  SSB_REQUIRE(pool && staging && blocks, "ssb_kv_hnd_copy: null pointer");
+  SSB_REQUIRE(l0 >= 0 && l0 + nl <= geo.n_layers && h0 >= 0 && h0 + nh <= geo.n_heads,
+              "ssb_kv_hnd_copy: rectangle outside the pool geometry");
+  SSB_REQUIRE(n_tokens <= n_blocks * geo.block_size, "ssb_kv_hnd_copy: %d tokens exceed %d blocks", n_tokens,
+              n_blocks);
+  if ((geo.head_dim * 2) % 16 || !aligned16(pool) || !aligned16(staging)) {
+    set_error("ssb_kv_hnd_copy: rows and buffers must be 16-byte aligned");
+    return SSB_EALIGN;
+  }
+  const int64_t runs = static_cast<int64_t>(nl) * 2 * nh * n_blocks;
+  SSB_REQUIRE(runs < (1ll << 31), "ssb_kv_hnd_copy: too many runs");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (gather)
+    kv_hnd_kernel<true><<<static_cast<int>(runs), kCopyThreads, 0, s>>>(
+        static_cast<uint8_t*>(pool), static_cast<uint8_t*>(staging), blocks, n_blocks, n_tokens, geo, l0, nl, h0,
+        nh);
+  else
+    kv_hnd_kernel<false><<<static_cast<int>(runs), kCopyThreads, 0, s>>>(
+        static_cast<uint8_t*>(pool), static_cast<uint8_t*>(staging), blocks, n_blocks, n_tokens, geo, l0, nl, h0,
+        nh);
+  return check_launch("ssb_kv_hnd_copy");
+}
 
 int ssb_kv_reshard_pack(const void* pool, ssb_kv_geometry geo, const int32_t* block_ids, int n_ids,
                         int n_peers, const int32_t* l0, const int32_t* nl, const int32_t* h0,

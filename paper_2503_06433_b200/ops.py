@@ -136,6 +136,23 @@ def copy2d_batched(src: torch.Tensor, dst: torch.Tensor, descs: torch.Tensor, to
     )
 
 
+def kv_hnd_copy(gather: bool, pool: torch.Tensor, geometry, blocks: torch.Tensor, n_tokens: int,
+                rect: tuple[int, int, int, int], staging: torch.Tensor, stream: int | None = None) -> None:
+    """One sequence's KV rectangle (l0, nl, h0, nh) between the pool and a
+    contiguous HND staging buffer [nl][2][nh][n_tokens][d] (host-tier swap)."""
+    if blocks.dtype != torch.int32 or not blocks.is_cuda:
+        raise ValueError("kv_hnd_copy: blocks must be a CUDA int32 tensor")
+    l0, nl, h0, nh = rect
+    call("ssb_kv_hnd_copy", 1 if gather else 0, pool.data_ptr(), _lib.KVGeometry(*geometry), blocks.data_ptr(),
+         blocks.numel(), n_tokens, l0, nl, h0, nh, staging.data_ptr(), stream if stream is not None else _stream())
+
+
+def memcpy2d_async(dst_ptr: int, dpitch: int, src_ptr: int, spitch: int, width: int, height: int,
+                   stream: int | None = None) -> None:
+    call("ssb_memcpy2d_async", dst_ptr, dpitch, src_ptr, spitch, width, height,
+         stream if stream is not None else _stream())
+
+
 def init_weights(arena: torch.Tensor, segs: torch.Tensor, total_elems: int, seed: int) -> None:
     """Counter-based init of ``arena`` (bf16) from a CUDA int64 [n, 8] segment table."""
     _check(arena, "arena")

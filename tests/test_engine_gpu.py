@@ -32,9 +32,10 @@ from paper_2503_06433_b200.specs import HardwareSpec, ParallelismConfig, Request
 pytestmark = pytest.mark.gpu
 
 
-def tiny_hw(n: int) -> HardwareSpec:
-    return HardwareSpec(num_gpus=n, hbm_bandwidth=8e12, peak_flops=2.25e15, gpu_memory=2e9,
-                        host_memory_per_gpu=2e9, host_link_bandwidth=64e9, allreduce=RingAllReduce(9e11))
+def tiny_hw(n: int, gpu_memory: float = 2e9, host_memory_per_gpu: float = 2e9) -> HardwareSpec:
+    return HardwareSpec(num_gpus=n, hbm_bandwidth=8e12, peak_flops=2.25e15, gpu_memory=gpu_memory,
+                        host_memory_per_gpu=host_memory_per_gpu, host_link_bandwidth=64e9,
+                        allreduce=RingAllReduce(9e11))
 
 
 def oracle_arch(a) -> lo.Arch:
@@ -63,11 +64,20 @@ def run_threads(n, fn):
     return out
 
 
-def _run_tiny(arch_name: str, cfg_p, cfg_d, n_req=8, s_in=64, s_out=32):
+def _run_tiny(arch_name: str, cfg_p, cfg_d, n_req=8, s_in=64, s_out=32, gpu_seqs=None):
     arch = PRESETS[arch_name]
     model = arch.model_spec()
     W = cfg_p.num_gpus
     hw = tiny_hw(W)
+    if gpu_seqs is not None:
+        # GPU tier sized to hold `gpu_seqs` full-size sequences (+ weights), the
+        # reference's sim_fleet trick (conftest.py:88-110): the rest must ride
+        # the host tier
+        from paper_2503_06433_b200.specs import kv_bytes_per_token, total_weight_bytes
+
+        k = (s_in + s_out) * kv_bytes_per_token(model)
+        hw = tiny_hw(W, gpu_memory=(total_weight_bytes(model) + gpu_seqs * k) / W,
+                     host_memory_per_gpu=n_req * k / W)
     reqs = [Request(i, s_in, s_out) for i in range(n_req)]
     prompts = synthetic_prompts(reqs, arch.vocab)
     comms = ThreadComm.create(W)
@@ -202,3 +212,35 @@ def test_logits_within_bf16_tolerance(tiny_run):
         for k, (g, e) in enumerate(zip(got, ref)):
             err = (g - e).abs().max().item()
             assert err <= 0.05 * e.abs().max().item() + 0.02, f"seq {r.id} step {k}: max err {err}"
+
+
+@pytest.fixture(scope="module")
+def tiered_run(cuda):
+    # GPU tier holds 3 sequences: 1 reserve for prefill staging + 2 residents;
+    # the other 6 prefill into the reserve, swap out and come back during decode
+    return _run_tiny("tiny", ParallelismConfig(1, 2, 1), ParallelismConfig(2, 1, 1), gpu_seqs=3)
+
+
+def test_host_tier_event_log(tiered_run):
+    arch, reqs, prompts, res, _ = tiered_run
+    rep = res[0][0]
+    assert rep.config["host_tier"]
+    assert replay_check(rep), replay_check(rep).violation
+    kinds = {}
+    for e in rep.event_log:
+        kinds[e.kind] = kinds.get(e.kind, 0) + 1
+    assert kinds["swap_out_complete"] == kinds["swap_in_start"] == kinds["swap_in_complete"] >= 1
+    assert kinds["prefill_complete"] == 8 and kinds["kv_release"] == 8 and rep.transitions == 1
+
+
+def test_host_tier_greedy_tokens(tiered_run):
+    arch, reqs, prompts, res, _ = tiered_run
+    check_greedy(arch, reqs, prompts, res[0][0].outputs, 1, 2)
+
+
+def test_host_tier_single_gpu(cuda):
+    arch, reqs, prompts, res, _ = _run_tiny("tiny", ParallelismConfig(1, 1, 1), ParallelismConfig(1, 1, 1),
+                                            gpu_seqs=2, n_req=6)
+    rep = res[0][0]
+    assert rep.config["host_tier"] and replay_check(rep)
+    check_greedy(arch, reqs, prompts, rep.outputs, 1, 1)
