@@ -238,6 +238,8 @@ def run_ours(args) -> None:
         "clocks": clocks,
         "decode_attention_hbm_frac": (da.get("gbs", 0) / peaks["hbm_gbs"]) if da else None,
     }
+    if n == 1:
+        line["reshard_micro"] = reshard_microbench(worker, arch, args, peaks)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, arch, sample_in=args.cpu_sample_in)
     print(json.dumps(line), flush=True)
@@ -245,6 +247,72 @@ def run_ours(args) -> None:
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def reshard_microbench(worker, arch, args, peaks, gpus: int = 8) -> dict:
+    """BASELINE configs[4] on one GPU: the per-GPU KV re-shard work of the 8B
+    batch at PP{gpus}->TP{gpus} (every resident block of one GPU: pack into
+    per-peer staging, unpack from staging into the decode geometry), timed per
+    kernel with CUDA events.  The NVLink transfer between the two needs peers;
+    at N=1 it is absent, so this reports the pack/unpack HBM rate and the
+    per-GPU NVLink floor the transfer would have (bytes leaving / 770 GB/s)."""
+    import torch
+
+    from paper_2503_06433_b200 import ops
+    from paper_2503_06433_b200.layout import kv_geometry
+    from paper_2503_06433_b200.reshard import kv_exchange
+    from paper_2503_06433_b200.specs import ParallelismConfig
+
+    bs = 64
+    blocks = args.prompts * (-(-(args.input_len + args.output_len) // bs))
+    src = kv_geometry(arch, 1, gpus, blocks, bs)
+    dst = kv_geometry(arch, gpus, 1, blocks, bs)
+    need = blocks * src.block_elems
+    pool = worker.pool[:need] if worker.pool is not None and worker.pool.numel() >= need else \
+        torch.empty(need, dtype=torch.bfloat16, device=worker.device)
+    ex = kv_exchange(arch.model_spec(), ParallelismConfig(1, gpus, 1), ParallelismConfig(gpus, 1, 1), 0)
+    cell = 2 * bs * arch.head_dim
+    chunk = 256
+    stage = torch.empty(chunk * src.block_elems + 8, dtype=torch.bfloat16, device=worker.device)
+
+    def peers(rects, nid):
+        out, off = [], 0
+        for r in rects:
+            out.append((r.l0, r.nl, r.h0, r.nh, off * 2))
+            off += nid * r.cells * cell
+        return out
+
+    ids_all = torch.arange(blocks, dtype=torch.int32, device=worker.device)
+    chunks = [ids_all[c : c + chunk] for c in range(0, blocks, chunk)]
+    # the loop-back stand-in: unpack every peer's segment from our own staging
+    t = {}
+    for name, fn in (("pack", lambda ids: ops.kv_reshard_pack(pool, src.as_tuple(), ids,
+                                                              peers(ex.send, ids.numel()), stage)),
+                     ("unpack", lambda ids: ops.kv_reshard_unpack(pool, dst.as_tuple(), ids,
+                                                                  peers(ex.recv, ids.numel()), stage))):
+        for ids in chunks[:2]:
+            fn(ids)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for ids in chunks:
+            fn(ids)
+        e.record()
+        torch.cuda.synchronize()
+        t[name] = s.elapsed_time(e) / 1e3
+    moved = need * 2  # bytes of KV this GPU holds
+    leaving = moved * (gpus - 1) // gpus
+    return {
+        "workload": f"{arch.name} KV of {args.prompts}x{args.input_len + args.output_len} tokens, "
+                    f"per-GPU share at PP{gpus}->TP{gpus} (BASELINE configs[4])",
+        "kv_bytes_per_gpu": moved, "bytes_leaving_gpu": leaving,
+        "pack_s": t["pack"], "unpack_s": t["unpack"],
+        "pack_hbm_gbs": 2 * moved / t["pack"] / 1e9, "unpack_hbm_gbs": 2 * moved / t["unpack"] / 1e9,
+        "pack_hbm_frac": 2 * moved / t["pack"] / 1e9 / peaks["hbm_gbs"],
+        "unpack_hbm_frac": 2 * moved / t["unpack"] / 1e9 / peaks["hbm_gbs"],
+        "nvlink_floor_s": leaving / 770e9,
+        "note": "transfer over NVLink not measurable with 1 GPU; pack+unpack overlap the all-to-all chunk by chunk",
+    }
 
 
 def profile_kernels(one, prompts, arch, args, dev, comm, world) -> dict:

@@ -49,7 +49,15 @@ int ssb_device_sm_count(void);
  * C[M,N] = A[M,K] . B[N,K]^T with A, B K-major.  block_n = 0 picks the tile.
  * ---------------------------------------------------------------------- */
 int ssb_gemm_bf16(const void* A, const void* B, void* C, const void* R, int M, int N, int K,
-                  int lda, int ldb, int ldc, int ldr, int epilogue, int block_n, void* stream);
+                  int lda, int ldb, int ldc, int ldr, int epilogue, int block_n, int max_ctas,
+                  void* stream);
+/* max_ctas > 0 caps the persistent grid (leaves SMs to a concurrent kernel,
+ * e.g. decode attention of the other half-batch); 0 = one CTA per SM.
+ * block_n bits 0-15: N tile (0 = auto: 128/192/224/256 by wave efficiency);
+ * OR in SSB_GEMM_MC2 for CTA pairs that share the B tile by TMA multicast
+ * (default single CTAs, SSB_GEMM_MC1). */
+#define SSB_GEMM_MC1 (1 << 16)
+#define SSB_GEMM_MC2 (1 << 17)
 
 /* ------------------------------------------------------------------------
  * KV re-shard between two parallelism layouts of the paged pool.

@@ -16,6 +16,8 @@ SSB_EPI_NONE = 0
 SSB_EPI_RESIDUAL = 1
 SSB_EPI_SILU_MUL = 2
 SSB_EPI_F32 = 3
+SSB_GEMM_MC1 = 1 << 16
+SSB_GEMM_MC2 = 1 << 17
 SSB_MAX_PEERS = 64
 
 
@@ -53,7 +55,7 @@ _PI64 = ctypes.POINTER(ctypes.c_int64)
 
 # name -> argtypes (restype is int for all compute entry points)
 SIGNATURES: dict[str, list] = {
-    "ssb_gemm_bf16": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P],
+    "ssb_gemm_bf16": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P],
     "ssb_kv_reshard_pack": [_P, KVGeometry, _P, _I, _I, _PI32, _PI32, _PI32, _PI32, _PI64, _P, _P],
     "ssb_kv_reshard_unpack": [_P, KVGeometry, _P, _I, _I, _PI32, _PI32, _PI32, _PI32, _PI64, _P, _P],
     "ssb_copy2d_batched": [_P, _P, _P, _I, _I64, _P],

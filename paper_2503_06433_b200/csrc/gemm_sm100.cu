@@ -17,6 +17,8 @@
 //   warps 2..5  epilogue: tcgen05.ld 32 lanes x 32 columns, fused epilogue,
 //               bf16 stores.  Accumulator double buffering lets the epilogue
 //               of tile i overlap the MMAs of tile i+1.
+#include <algorithm>
+
 #include "common.cuh"
 #include "seesaw_b200.h"
 
@@ -33,13 +35,16 @@ constexpr int kUmmaK = 16;
 constexpr int kThreads = 192;
 constexpr int kGroupM = 16;   // tile rasterisation: 16 M-tiles share a B band in L2
 
+constexpr int pow2_at_least(int x) { return x <= 32 ? 32 : x <= 64 ? 64 : x <= 128 ? 128 : x <= 256 ? 256 : 512; }
+
 template <int BN>
 struct Cfg {
-  static constexpr int kStages = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+  // as many stages as ~220 KB of shared memory holds (>= 4)
+  static constexpr int kStages = (220 * 1024) / kStageBytes > 8 ? 8 : (220 * 1024) / kStageBytes;
+  static constexpr int kTmemCols = pow2_at_least(2 * BN);
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
@@ -72,11 +77,21 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
 
-template <int BN>
+// MC = CTAs per cluster along M.  With MC = 2 the two CTAs of a cluster
+// compute vertically adjacent M tiles of the same N tile: each loads its own
+// A tile and HALF of the shared B tile, multicast into both CTAs' smem
+// (TMA .multicast::cluster), halving B's L2->SM traffic.  A stage may be
+// refilled only when both CTAs' MMAs released it, so MMA completion is
+// committed to the empty barrier of both CTAs.
+template <int BN, int MC>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmap_a,
                     const __grid_constant__ CUtensorMap tmap_b, const Params p) {
   using C = Cfg<BN>;
+  const int crank = MC > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+  const int cid = blockIdx.x / MC;
+  const int nclusters = gridDim.x / MC;
+  const int units_m = (p.tiles_m + MC - 1) / MC;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the SW128 atoms.
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -92,7 +107,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int num_tiles = p.tiles_m * p.tiles_n;
+  const int num_units = units_m * p.tiles_n;
   const int num_kb = (p.K + kBK - 1) / kBK;
 
   if (warp == 0 && lane == 0) {
@@ -100,7 +115,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tmap_b);
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC);  // both CTAs' MMAs must release a multicast stage
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -111,6 +126,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
   tc_fence_before();
   __syncthreads();
+  if (MC > 1) cluster_sync_all();  // peer barriers initialised before any multicast lands
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -123,16 +139,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_b = p.group_n ? policy_evict_last() : policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        int tm, tn;
-        tile_coords(t, p.tiles_m, p.tiles_n, p.group_n, tm, tn);
+      for (int u = cid; u < num_units; u += nclusters) {
+        int um, tn;
+        tile_coords(u, units_m, p.tiles_n, p.group_n, um, tn);
+        const int tm = um * MC + crank;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
           tma_load_2d(smem_a + stage * C::kABytes, &tmap_a, &full[stage], kb * kBK, tm * kBM,
                       pol_a);
-          tma_load_2d(smem_b + stage * C::kBBytes, &tmap_b, &full[stage], kb * kBK, tn * BN,
-                      pol_b);
+          if (MC == 1) {
+            tma_load_2d(smem_b + stage * C::kBBytes, &tmap_b, &full[stage], kb * kBK, tn * BN,
+                        pol_b);
+          } else {
+            // my half of the B tile, written into both CTAs of the cluster
+            tma_load_2d_mc(smem_b + stage * C::kBBytes + crank * (C::kBBytes / MC), &tmap_b, &full[stage],
+                           kb * kBK, tn * BN + crank * (BN / MC), static_cast<uint16_t>((1u << MC) - 1), pol_b);
+          }
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
@@ -148,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int u = cid; u < num_units; u += nclusters) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -162,7 +185,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             // advance 16 elements (32 B) along K inside the 128 B swizzle row
             umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
           }
-          umma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
+          // frees the smem slot (in every CTA that received multicast into it)
+          if (MC == 1)
+            umma_commit(&empty[stage]);
+          else
+            umma_commit_mc(&empty[stage], static_cast<uint16_t>((1u << MC) - 1));
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
@@ -178,9 +205,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      int tm, tn;
-      tile_coords(t, p.tiles_m, p.tiles_n, p.group_n, tm, tn);
+    for (int u = cid; u < num_units; u += nclusters) {
+      int um, tn;
+      tile_coords(u, units_m, p.tiles_n, p.group_n, um, tn);
+      const int tm = um * MC + crank;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = tm * kBM + q * 32 + lane;
@@ -293,25 +321,29 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+  // no CTA leaves while its peer may still multicast into it / arrive on it
+  if (MC > 1) cluster_sync_all();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::kTmemCols);
   }
 }
 
-template <int BN>
+template <int BN, int MC>
 int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, int K, int lda,
            int ldb, int ldc, int ldr, int epi, cudaStream_t stream, int max_ctas) {
   using C = Cfg<BN>;
   CUtensorMap ta, tb;
   int rc = encode_tmap_2d_bf16(&ta, A, K, M, static_cast<uint64_t>(lda) * 2, kBK, kBM);
   if (rc) return rc;
-  rc = encode_tmap_2d_bf16(&tb, B, K, N, static_cast<uint64_t>(ldb) * 2, kBK, BN);
+  rc = encode_tmap_2d_bf16(&tb, B, K, N, static_cast<uint64_t>(ldb) * 2, kBK, BN / MC);
   if (rc) return rc;
-  static bool attr_done = false;  // per BN instantiation
+  static bool attr_done = false;  // per <BN, MC> instantiation
   if (!attr_done) {
-    SSB_CUDA(cudaFuncSetAttribute(gemm_bf16_sm100<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SSB_CUDA(cudaFuncSetAttribute(gemm_bf16_sm100<BN, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   C::kSmemBytes));
+    if (MC > 1)
+      SSB_CUDA(cudaFuncSetAttribute(gemm_bf16_sm100<BN, MC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr_done = true;
   }
   Params p;
@@ -333,20 +365,52 @@ int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, 
     const double n_band = b_bytes + a_bytes * ((p.tiles_n + kGroupM - 1) / kGroupM);
     p.group_n = n_band < m_band ? 1 : 0;
   }
-  const int tiles = p.tiles_m * p.tiles_n;
+  const int units = ((p.tiles_m + MC - 1) / MC) * p.tiles_n;
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
-  if (tiles < grid) grid = tiles;
-  gemm_bf16_sm100<BN><<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, p);
+  grid = std::min(grid / MC, units) * MC;
+  if (MC == 1) {
+    gemm_bf16_sm100<BN, 1><<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, p);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = MC;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SSB_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_sm100<BN, MC>, ta, tb, p));
+  }
   return check_launch("gemm_bf16_sm100");
 }
 
-// Pick the widest N tile that still fills the machine.
-int choose_bn(int M, int N, int sms) {
+// Pick the N tile maximising wave efficiency (tiles / (waves * SMs)),
+// weighted by the per-tile efficiency of wider tiles (A-tile reuse).
+int choose_bn(int M, int N, int sms, int epi) {
   const int tm = (M + kBM - 1) / kBM;
-  const long t256 = static_cast<long>(tm) * ((N + 255) / 256);
-  if (t256 >= sms) return 256;
-  return 128;
+  const int cands[4] = {256, 224, 192, 128};
+  const double weight[4] = {1.0, 0.985, 0.97, 0.93};
+  int best = 256;
+  double best_score = -1.0;
+  for (int i = 0; i < 4; ++i) {
+    const int bn = cands[i];
+    if (epi == SSB_EPI_SILU_MUL && bn % 64) continue;  // gate/up pairs of 32 columns
+    const long tiles = static_cast<long>(tm) * ((N + bn - 1) / bn);
+    const long waves = (tiles + sms - 1) / sms;
+    // columns past N are wasted MMA work
+    const double fill = static_cast<double>(N) / (static_cast<double>((N + bn - 1) / bn) * bn);
+    const double score = static_cast<double>(tiles) / (waves * sms) * weight[i] * fill;
+    if (score > best_score + 1e-9) {
+      best_score = score;
+      best = bn;
+    }
+  }
+  return best;
 }
 
 }  // namespace
@@ -354,7 +418,7 @@ int choose_bn(int M, int N, int sms) {
 
 extern "C" int ssb_gemm_bf16(const void* A, const void* B, void* C, const void* R, int M, int N,
                              int K, int lda, int ldb, int ldc, int ldr, int epilogue, int block_n,
-                             void* stream) {
+                             int max_ctas, void* stream) {
   using namespace ssb;
   SSB_REQUIRE(M > 0 && N > 0 && K > 0, "ssb_gemm_bf16: empty problem M=%d N=%d K=%d", M, N, K);
   SSB_REQUIRE(A && B && C, "ssb_gemm_bf16: null operand");
@@ -371,12 +435,26 @@ extern "C" int ssb_gemm_bf16(const void* A, const void* B, void* C, const void* 
     return SSB_EALIGN;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  int bn = block_n;
-  if (bn == 0) bn = choose_bn(M, epilogue == SSB_EPI_SILU_MUL ? N : N, num_sms());
+  // block_n: bits 0-15 tile width (0 = auto); SSB_GEMM_MC1 / SSB_GEMM_MC2
+  // force the cluster size (default: pairs whenever there are >= 2 M tiles)
+  int bn = block_n & 0xFFFF;
+  // measured on B200 (tools/bench_kernels.py --what mc): B multicast across a
+  // CTA pair is 2-8% SLOWER than single CTAs on the Llama shapes (L2->SM
+  // bandwidth is not the limiter), so pairs are opt-in
+  int mc = (block_n & SSB_GEMM_MC2) ? 2 : 1;
+  if (bn == 0) bn = choose_bn(M, N, max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms(), epilogue);
+  if (epilogue == SSB_EPI_SILU_MUL && bn % 64) return fail_arg("ssb_gemm_bf16: SiLU epilogue needs block_n %% 64 == 0");
+#define SSB_GEMM_CASE(BN_)                                                                              \
+  case BN_:                                                                                            \
+    return mc == 2 ? launch<BN_, 2>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas)   \
+                   : launch<BN_, 1>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas);
   switch (bn) {
-    case 256: return launch<256>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, 0);
-    case 128: return launch<128>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, 0);
-    case 64: return launch<64>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, 0);
-    default: return fail_arg("ssb_gemm_bf16: block_n must be 0, 64, 128 or 256 (got %d)", block_n);
+    SSB_GEMM_CASE(256)
+    SSB_GEMM_CASE(224)
+    SSB_GEMM_CASE(192)
+    SSB_GEMM_CASE(128)
+    SSB_GEMM_CASE(64)
+    default: return fail_arg("ssb_gemm_bf16: block_n must be 0, 64, 128, 192, 224 or 256 (got %d)", bn);
   }
+#undef SSB_GEMM_CASE
 }

@@ -34,6 +34,7 @@ def gemm(
     silu_mul: bool = False,
     block_n: int = 0,
     out_f32: bool = False,
+    max_ctas: int = 0,
 ) -> torch.Tensor:
     """out = a @ w.T (+ residual) or silu-mul of interleaved gate/up columns,
     or fp32 output (logits) with ``out_f32``.
@@ -74,6 +75,7 @@ def gemm(
         residual.stride(0) if residual is not None else 0,
         epi,
         block_n,
+        max_ctas,
         _stream(),
     )
     return out

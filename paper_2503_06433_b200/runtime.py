@@ -110,6 +110,17 @@ class Worker:
         self.stats: dict[str, float] = {}
         # test/inspection callbacks invoked by the engine: name -> fn(worker, **kw)
         self.hooks: dict = {}
+        self._bufs: dict = {}
+        self._side = None
+        # decode overlap: two half-batch lanes on two streams; GEMM grid cap
+        import os
+
+        # measured on B200 (tools/bench_decode.py, 8B, B=512): two lanes are
+        # ~3% SLOWER than one (the second weight read outweighs the overlap),
+        # so the overlap is off by default
+        self.decode_lanes = int(os.environ.get("SSB_DECODE_LANES", "1"))
+        self.lane_gemm_cap = int(os.environ.get("SSB_LANE_GEMM_CAP", "0"))
+        self.min_lane_rows = int(os.environ.get("SSB_MIN_LANE_ROWS", "64"))
 
     # ------------------------------------------------------------ layouts --
     def _tp_comm(self, cfg: ParallelismConfig, stage: int) -> Comm:
@@ -212,12 +223,15 @@ class Worker:
         max_cells_s = sum(r.cells for r in ex.send)
         max_cells_r = sum(r.cells for r in ex.recv)
         chunk = min(chunk_blocks, ids_all.size)
-        send = torch.empty(chunk * max_cells_s * cell + 8, dtype=torch.bfloat16, device=self.device)
-        recv = torch.empty(chunk * max_cells_r * cell + 8, dtype=torch.bfloat16, device=self.device)
-        for c0 in range(0, ids_all.size, chunk):
+        nbuf = 2 if self.device.type == "cuda" else 1
+        sends = [torch.empty(chunk * max_cells_s * cell + 8, dtype=torch.bfloat16, device=self.device)
+                 for _ in range(nbuf)]
+        recvs = [torch.empty(chunk * max_cells_r * cell + 8, dtype=torch.bfloat16, device=self.device)
+                 for _ in range(nbuf)]
+
+        def plan(c0):
             ids_np = ids_all[c0 : c0 + chunk]
             nid = ids_np.size
-            ids = torch.from_numpy(ids_np).to(self.device)
             s_peers, r_peers, s_splits, r_splits = [], [], [], []
             so = ro = 0
             for q in range(self.per_replica):
@@ -228,10 +242,46 @@ class Worker:
                 r_splits.append(nid * rr.cells * cell)
                 so += s_splits[-1]
                 ro += r_splits[-1]
-            ops.kv_reshard_pack(self.pool, geo_s.as_tuple(), ids, s_peers, send)
-            self.replica_comm.all_to_all(recv, send, r_splits, s_splits)
-            ops.kv_reshard_unpack(self.pool, geo_d.as_tuple(), ids, r_peers, recv)
+            return torch.from_numpy(ids_np).to(self.device), s_peers, r_peers, s_splits, r_splits, so
+
+        chunks = [plan(c0) for c0 in range(0, ids_all.size, chunk)]
+        for _, _, _, s_splits, _, so in chunks:
             sent += 2 * (so - s_splits[self.gpu])
+        if nbuf == 1:  # host (gloo) path: strictly sequential
+            for ids, s_peers, r_peers, s_splits, r_splits, _ in chunks:
+                ops.kv_reshard_pack(self.pool, geo_s.as_tuple(), ids, s_peers, sends[0])
+                self.replica_comm.all_to_all(recvs[0], sends[0], r_splits, s_splits)
+                ops.kv_reshard_unpack(self.pool, geo_d.as_tuple(), ids, r_peers, recvs[0])
+            return sent
+        # software pipeline over chunks: pack(i+1) on the compute stream and
+        # all-to-all(i) on the comm stream overlap; unpack(i) waits for its
+        # transfer.  Chunks are disjoint block sets, so packing chunk i+1 from
+        # the old layout while unpacking chunk i into the new one is safe.
+        main = torch.cuda.current_stream(self.device)
+        if getattr(self, "_comm_stream", None) is None:
+            self._comm_stream = torch.cuda.Stream(self.device)
+        cs = self._comm_stream
+        arrived: list = [None] * len(chunks)
+
+        def launch(i):
+            ids, s_peers, _, s_splits, r_splits, _ = chunks[i]
+            b = i % nbuf
+            ops.kv_reshard_pack(self.pool, geo_s.as_tuple(), ids, s_peers, sends[b])
+            packed = torch.cuda.Event()
+            packed.record(main)
+            with torch.cuda.stream(cs):
+                cs.wait_event(packed)
+                self.replica_comm.all_to_all(recvs[b], sends[b], r_splits, s_splits)
+                arrived[i] = torch.cuda.Event()
+                arrived[i].record(cs)
+
+        launch(0)
+        for i in range(len(chunks)):
+            if i + 1 < len(chunks):
+                launch(i + 1)
+            ids, _, r_peers, _, _, _ = chunks[i]
+            main.wait_event(arrived[i])
+            ops.kv_reshard_unpack(self.pool, geo_d.as_tuple(), ids, r_peers, recvs[i % nbuf])
         return sent
 
     # ------------------------------------------------------------- forward --
@@ -239,20 +289,21 @@ class Worker:
         wl = self.state.weights
         return range(wl.layer_begin, wl.layer_end)
 
-    def _block(self, x: torch.Tensor, layer: int, attn_fn, buf: dict) -> None:
-        """One transformer layer on x (in place); attn_fn(qkv, layer_local) -> attn out."""
+    def _block(self, x: torch.Tensor, layer: int, attn_fn, buf: dict, cap: int = 0) -> None:
+        """One transformer layer on x (in place); attn_fn(qkv, layer_local) -> attn out.
+        ``cap`` bounds the GEMMs' persistent grid (decode lane overlap)."""
         st = self.state
         eps = self.arch.rms_eps
         p = f"L{layer}."
         lead = st.rank == 0
         h = ops.rmsnorm(x, self.w(p + "attn_norm"), eps, out=buf["h"])
-        qkv = ops.gemm(h, self.w(p + "wqkv"), out=buf["qkv"])
+        qkv = ops.gemm(h, self.w(p + "wqkv"), out=buf["qkv"], max_ctas=cap)
         attn = attn_fn(qkv, layer - st.weights.layer_begin)
-        ops.gemm(attn, self.w(p + "wo"), out=x, residual=x if lead else None)
+        ops.gemm(attn, self.w(p + "wo"), out=x, residual=x if lead else None, max_ctas=cap)
         self._reduce_into(x)
         h = ops.rmsnorm(x, self.w(p + "mlp_norm"), eps, out=buf["h"])
-        act = ops.gemm(h, self.w(p + "w13"), out=buf["act"], silu_mul=True)
-        ops.gemm(act, self.w(p + "w2"), out=x, residual=x if lead else None)
+        act = ops.gemm(h, self.w(p + "w13"), out=buf["act"], silu_mul=True, max_ctas=cap)
+        ops.gemm(act, self.w(p + "w2"), out=x, residual=x if lead else None, max_ctas=cap)
         self._reduce_into(x)
 
     def _reduce_into(self, x: torch.Tensor) -> None:
@@ -261,21 +312,23 @@ class Worker:
         if self.state.tp_comm.size > 1:
             self.state.tp_comm.all_reduce_(x)
 
-    def _buffers(self, T: int) -> dict:
+    def _buffers(self, T: int, lane: int = 0) -> dict:
+        """Activation buffers of a T-row forward, one set per decode lane."""
         st = self.state
         a = self.arch
         nq, nk = st.weights.n_q_heads, st.weights.n_kv_heads
         key = ("buf", T, st.cfg.tp)
-        if self._comm_cache.get("buf_key") != key:
+        slot = self._bufs.setdefault(lane, {})
+        if slot.get("key") != key:
             dev = self.device
-            self._comm_cache["buf"] = {
+            slot["key"] = key
+            slot["buf"] = {
                 "h": torch.empty(T, a.hidden, dtype=torch.bfloat16, device=dev),
                 "qkv": torch.empty(T, (nq + 2 * nk) * a.head_dim, dtype=torch.bfloat16, device=dev),
                 "attn": torch.empty(T, nq * a.head_dim, dtype=torch.bfloat16, device=dev),
                 "act": torch.empty(T, st.weights.ffn_local, dtype=torch.bfloat16, device=dev),
             }
-            self._comm_cache["buf_key"] = key
-        return self._comm_cache["buf"]
+        return slot["buf"]
 
     def _logits_argmax(self, h_last: torch.Tensor, out_tokens: torch.Tensor) -> None:
         """Vocab-parallel LM head + greedy argmax (fp32 logits)."""
@@ -354,28 +407,61 @@ class Worker:
     def decode_step(self, tokens: torch.Tensor, ctx_lens: torch.Tensor, tables: torch.Tensor,
                     positions: torch.Tensor, slots: torch.Tensor, out_tokens: torch.Tensor) -> None:
         """One decode step of the resident batch under a pure-TP layout:
-        tokens[B] in, next greedy tokens into out_tokens[B]; ctx_lens grows by one."""
+        tokens[B] in, next greedy tokens into out_tokens[B]; ctx_lens grows by one.
+
+        With ``decode_lanes == 2`` the batch is split into two halves issued on
+        two CUDA streams, layer by layer: one half's paged attention (HBM
+        bound) runs while the other half's projections (tensor bound) run on
+        the SMs the capped persistent GEMM leaves free."""
+        B = tokens.numel()
+        lanes = self.decode_lanes if (B >= 2 * self.min_lane_rows and not self.record_logits) else 1
+        if lanes == 1:
+            self._decode_lanes([(0, B)], tokens, ctx_lens, tables, positions, slots, out_tokens, 0)
+            return
+        h = B // 2
+        self._decode_lanes([(0, h), (h, B)], tokens, ctx_lens, tables, positions, slots, out_tokens,
+                           self.lane_gemm_cap)
+
+    def _decode_lanes(self, spans, tokens, ctx_lens, tables, positions, slots, out_tokens, cap) -> None:
         st = self.state
         a = self.arch
-        B = tokens.numel()
-        buf = self._buffers(B)
-        x = buf.setdefault("x", torch.empty(B, a.hidden, dtype=torch.bfloat16, device=self.device))
-        if x.shape[0] != B:
-            x = buf["x"] = torch.empty(B, a.hidden, dtype=torch.bfloat16, device=self.device)
-        ops.decode_positions(ctx_lens, tables, self.block_size, positions, slots)
-        ops.embedding(tokens, self.w("embed"), st.weights.vocab_begin, x)
-        if st.tp_comm.size > 1:
-            st.tp_comm.all_reduce_(x)
+        main = torch.cuda.current_stream(self.device)
+        if len(spans) > 1:
+            if self._side is None:
+                self._side = torch.cuda.Stream(self.device)
+            self._side.wait_stream(main)
+        streams = [main] + [self._side] * (len(spans) - 1)
         geo = self.geometry()
         nq, nk = st.weights.n_q_heads, st.weights.n_kv_heads
+        lanes = []
+        for li, ((b0, b1), s) in enumerate(zip(spans, streams)):
+            with torch.cuda.stream(s):
+                n = b1 - b0
+                buf = self._buffers(n, lane=li)
+                x = buf.get("x")
+                if x is None or x.shape[0] != n:
+                    x = buf["x"] = torch.empty(n, a.hidden, dtype=torch.bfloat16, device=self.device)
+                v = dict(tok=tokens[b0:b1], ctx=ctx_lens[b0:b1], tab=tables[b0:b1], pos=positions[b0:b1],
+                         slot=slots[b0:b1], out=out_tokens[b0:b1])
+                ops.decode_positions(v["ctx"], v["tab"], self.block_size, v["pos"], v["slot"])
+                ops.embedding(v["tok"], self.w("embed"), st.weights.vocab_begin, x)
+                if st.tp_comm.size > 1:
+                    st.tp_comm.all_reduce_(x)
 
-        def attn(qkv, layer_local):
-            ops.rope_kv_append(qkv, nq, nk, positions, self.rope_cos, self.rope_sin, self.pool, geo.as_tuple(),
-                               layer_local, slots)
-            return ops.decode_attention(qkv, nq, nk, self.pool, geo.as_tuple(), self.num_blocks, layer_local,
-                                        tables, ctx_lens, buf["attn"], self.scale)
+                def attn(qkv, layer_local, v=v, buf=buf):
+                    ops.rope_kv_append(qkv, nq, nk, v["pos"], self.rope_cos, self.rope_sin, self.pool,
+                                       geo.as_tuple(), layer_local, v["slot"])
+                    return ops.decode_attention(qkv, nq, nk, self.pool, geo.as_tuple(), self.num_blocks,
+                                                layer_local, v["tab"], v["ctx"], buf["attn"], self.scale)
 
+                lanes.append((s, x, attn, buf, v))
         for layer in self._layers():
-            self._block(x, layer, attn, buf)
-        h = ops.rmsnorm(x, self.w("final_norm"), a.rms_eps, out=buf["h"])
-        self._logits_argmax(h, out_tokens)
+            for s, x, attn, buf, _ in lanes:
+                with torch.cuda.stream(s):
+                    self._block(x, layer, attn, buf, cap)
+        for s, x, _, buf, v in lanes:
+            with torch.cuda.stream(s):
+                h = ops.rmsnorm(x, self.w("final_norm"), a.rms_eps, out=buf["h"])
+                self._logits_argmax(h, v["out"])
+        if len(spans) > 1:
+            main.wait_stream(self._side)

@@ -24,6 +24,10 @@ def _ref(a, w):
         (77, 200, 136, 64),
         (300, 384, 1024, 128),
         (4096, 4096, 4096, 256),
+        (512, 6144, 4096, 192),
+        (512, 4096, 4096, 224),
+        (300, 200, 136, 224),
+        (130, 1000, 520, 192),
     ],
 )
 def test_gemm_plain(cuda, M, N, K, bn):
@@ -38,6 +42,21 @@ def test_gemm_plain(cuda, M, N, K, bn):
     assert err <= tol, f"max err {err} > {tol}"
 
 
+@pytest.mark.parametrize("mc", [1, 2])
+@pytest.mark.parametrize("M,N,K,bn", [(300, 640, 512, 128), (512, 4096, 1024, 192), (1000, 768, 4096, 256),
+                                      (129, 448, 256, 224), (64, 256, 128, 128)])
+def test_gemm_cluster_multicast(cuda, mc, M, N, K, bn):
+    from paper_2503_06433_b200._lib import SSB_GEMM_MC1, SSB_GEMM_MC2
+
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    a = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=cuda, generator=g) / K**0.5).to(torch.bfloat16)
+    out = ops.gemm(a, w, block_n=bn | (SSB_GEMM_MC2 if mc == 2 else SSB_GEMM_MC1))
+    torch.cuda.synchronize()
+    ref = _ref(a, w)
+    assert (out.float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item() + 1e-2
+
+
 def test_gemm_residual_inplace(cuda):
     M, N, K = 384, 1024, 512
     a = torch.randn(M, K, device=cuda).to(torch.bfloat16)
@@ -49,14 +68,15 @@ def test_gemm_residual_inplace(cuda):
     assert (r.float() - ref).abs().max().item() < 5e-2
 
 
-def test_gemm_silu_mul(cuda):
-    M, F, K = 640, 512, 1024
+@pytest.mark.parametrize("bn", [0, 128, 192, 256])
+def test_gemm_silu_mul(cuda, bn):
+    M, F, K = 640, 480, 1024
     a = torch.randn(M, K, device=cuda).to(torch.bfloat16)
     gate = (torch.randn(F, K, device=cuda) / K**0.5).to(torch.bfloat16)
     up = (torch.randn(F, K, device=cuda) / K**0.5).to(torch.bfloat16)
     # interleave (32 gate, 32 up) row groups
     w = torch.stack([gate.view(F // 32, 32, K), up.view(F // 32, 32, K)], dim=1).reshape(2 * F, K)
-    out = ops.gemm(a, w, silu_mul=True)
+    out = ops.gemm(a, w, silu_mul=True, block_n=bn)
     torch.cuda.synchronize()
     g = a.float() @ gate.float().T
     u = a.float() @ up.float().T

@@ -41,7 +41,7 @@ def test_ctypes_signatures_cover_header():
 
 def test_argument_errors_are_reported_not_raised():
     lib = _lib.load()
-    rc = lib.ssb_gemm_bf16(None, None, None, None, 0, 0, 0, 0, 0, 0, 0, 0, 0, None)
+    rc = lib.ssb_gemm_bf16(None, None, None, None, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, None)
     assert rc < 0
     assert b"empty problem" in lib.ssb_last_error()
     with pytest.raises(_lib.SeesawKernelError, match="n_peers"):

@@ -56,6 +56,11 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--what", default="gemm")
     args = ap.parse_args()
+    if args.what == "mc":
+        MC1, MC2 = 1 << 16, 1 << 17
+        shapes = [(8192, 6144, 4096), (8192, 28672, 4096), (8192, 4096, 14336), (512, 6144, 4096),
+                  (512, 4096, 4096), (512, 28672, 4096), (512, 4096, 14336), (512, 128256, 4096)]
+        bench_gemm([(M, N, K, MC1) for M, N, K in shapes] + [(M, N, K, MC2) for M, N, K in shapes])
     if args.what == "gemm":
         bench_gemm([
             (8192, 6144, 4096, 256), (8192, 4096, 4096, 256), (8192, 28672, 4096, 256),
