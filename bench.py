@@ -235,6 +235,7 @@ def run_ours(args) -> None:
                     "gbs_per_gpu": (rep.measured.get("reshard_bytes_sent", 0) / reshard_s / 1e9) if reshard_s else None,
                     "share_of_e2e": reshard_s / rep.makespan},
         "replay_check": bool(verdict),
+        "reference_model_prediction": _predict(model, hw, cfg_p, cfg_d, args),
         "clocks": clocks,
         "decode_attention_hbm_frac": (da.get("gbs", 0) / peaks["hbm_gbs"]) if da else None,
     }
@@ -247,6 +248,16 @@ def run_ours(args) -> None:
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def _predict(model, hw, cfg_p, cfg_d, args) -> dict:
+    """The reference's analytic model (perf.py restated) on the same B200
+    HardwareSpec: what shardsim.simulate would charge for this batch."""
+    from paper_2503_06433_b200.perf import predict_phases
+
+    p = predict_phases(model, hw, cfg_p, cfg_d, args.input_len, args.output_len, args.prompts)
+    p["tokens_per_s"] = args.prompts * args.output_len / (p["prefill_s"] + p["decode_s"])
+    return p
 
 
 def reshard_microbench(worker, arch, args, peaks, gpus: int = 8) -> dict:

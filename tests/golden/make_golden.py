@@ -177,7 +177,33 @@ def sim_golden() -> dict:
     return {"runs": out}
 
 
+def perf_golden() -> dict:
+    """Reference cost-model values (perf.py) the restated model must equal."""
+    from shardsim import perf
+    from shardsim.perf import Mode, Phase
+
+    out = []
+    rnd = random.Random(11)
+    for (m, cfg) in random_cases(60, 3) + [(SHAPES["llama3-8b"], ParallelismConfig(8, 1, 1)),
+                                          (SHAPES["llama3-8b"], ParallelismConfig(1, 8, 1))]:
+        hw = b200_fleet(cfg.num_gpus)
+        for phase in (Phase.PREFILL, Phase.DECODE):
+            for mode in (Mode.ROOFLINE, Mode.ADDITIVE):
+                b, s = rnd.choice([1, 3, 16]), rnd.choice([1, 17, 1024])
+                lens = [rnd.randint(1, 600) for _ in range(rnd.randint(1, 5))]
+                out.append({
+                    "model": model_doc(m), "hw": hw_doc(hw), "cfg": [cfg.tp, cfg.pp, cfg.dp], "phase": phase.value,
+                    "mode": mode.value, "b": b, "s": s, "lens": lens,
+                    "layer": perf.layer_time(m, hw, cfg, b, s, phase, mode).as_dict(),
+                    "batch": perf.layer_time_batch(m, hw, cfg, lens, phase, mode).as_dict(),
+                    "stage": perf.stage_time(m, hw, cfg, b * 4, s, phase, mode),
+                    "tinv": perf.throughput_inverse(m, hw, cfg, b * 4, s, phase, mode),
+                })
+    return {"cases": out}
+
+
 def main() -> None:
+    (OUT / "perf.json").write_text(json.dumps(perf_golden(), sort_keys=True))
     (OUT / "planning.json").write_text(json.dumps(planning_golden(), sort_keys=True))
     (OUT / "simulate.json").write_text(json.dumps(sim_golden(), sort_keys=True))
     print("wrote", OUT / "planning.json", OUT / "simulate.json", "with shardsim", shardsim.__version__)

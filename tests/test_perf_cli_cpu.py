@@ -1,0 +1,67 @@
+"""Restated cost model == reference perf.py (golden), and the CLI's
+plan/predict/error paths (cli.py conventions: JSON errors, exit 1)."""
+
+from __future__ import annotations
+
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+from paper_2503_06433_b200 import ModelSpec, ParallelismConfig
+from paper_2503_06433_b200 import perf
+from paper_2503_06433_b200.cli import TraceError, main, parse_trace
+from paper_2503_06433_b200.report import Mode
+from paper_2503_06433_b200.specs import hardware_spec_from_mapping
+
+ROOT = Path(__file__).resolve().parent.parent
+GOLD = json.loads((ROOT / "tests" / "golden" / "perf.json").read_text())
+
+
+def test_cost_model_matches_reference():
+    assert len(GOLD["cases"]) > 100
+    for c in GOLD["cases"]:
+        m = ModelSpec(**c["model"])
+        hw = hardware_spec_from_mapping(c["hw"])
+        cfg = ParallelismConfig(*c["cfg"])
+        ph, mode = perf.Phase(c["phase"]), Mode(c["mode"])
+        assert perf.layer_time(m, hw, cfg, c["b"], c["s"], ph, mode).as_dict() == pytest.approx(c["layer"], rel=1e-12)
+        assert perf.layer_time_batch(m, hw, cfg, c["lens"], ph, mode).as_dict() == pytest.approx(c["batch"], rel=1e-12)
+        assert perf.stage_time(m, hw, cfg, c["b"] * 4, c["s"], ph, mode) == pytest.approx(c["stage"], rel=1e-12)
+        assert perf.throughput_inverse(m, hw, cfg, c["b"] * 4, c["s"], ph, mode) == pytest.approx(c["tinv"], rel=1e-12)
+
+
+def test_cli_plan_and_predict(capsys):
+    args = ["--model", str(ROOT / "configs/model_llama3_8b.yaml"), "--hw", str(ROOT / "configs/b200_x8.yaml")]
+    assert main(["plan", *args, "--cfg", "tp1.pp8", "--new-cfg", "tp8.pp1", "--tokens", "1"]) == 0
+    out = capsys.readouterr().out
+    doc = json.loads(out[out.index("{"):])
+    mat = doc["nvlink_kv_exchange_bytes"]
+    assert len(mat) == 8 and all(v == 2048 for row in mat for v in row)  # 16 KiB/token split 8 ways
+    assert main(["predict", *args, "--prefill-cfg", "tp1.pp8", "--decode-cfg", "tp8.pp1", "--prompts", "512",
+                 "--input-len", "1024", "--output-len", "256"]) == 0
+    pred = json.loads(capsys.readouterr().out)
+    assert pred["prefill_s"] > 0 and pred["decode_s"] > 0
+
+
+def test_cli_errors_are_json(tmp_path):
+    bad = tmp_path / "t.jsonl"
+    bad.write_text('{"input_len": 4}\n')
+    with pytest.raises(TraceError):
+        parse_trace(bad)
+    proc = subprocess.run([sys.executable, "-m", "paper_2503_06433_b200", "plan", "--model",
+                           str(ROOT / "configs/model_llama3_8b.yaml"), "--hw", str(ROOT / "configs/b200_x8.yaml"),
+                           "--cfg", "tp3.pp1"], capture_output=True, text=True, cwd=ROOT)
+    assert proc.returncode == 1
+    err = json.loads(proc.stderr.strip().splitlines()[-1])
+    assert err["error_kind"] == "ConfigError" and "tp=3" in err["message"]
+
+
+def test_trace_with_prompts(tmp_path):
+    t = tmp_path / "t.jsonl"
+    t.write_text('{"id": "a", "input_len": 3, "output_len": 2, "prompt": [1, 2, 3]}\n'
+                 '{"input_len": 2, "output_len": 1, "prompt": [5, 6]}\n')
+    reqs, prompts = parse_trace(t)
+    assert [r.id for r in reqs] == ["a", 1] and prompts == [[1, 2, 3], [5, 6]]
