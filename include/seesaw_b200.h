@@ -199,11 +199,13 @@ int ssb_argmax_combine(const float* vals, const int32_t* idxs, int n_parts, int 
  * Attention.  Replaces perf.py:68-89 / :92-111 (attention traffic and
  * compute) in _quantum (sim.py:335-341).
  * ---------------------------------------------------------------------- */
-/* Causal prefill over packed sequences: qkv[T, (nq+2nk)*d] (RoPE applied),
- * sequence s spans rows [cu_seqlens[s], cu_seqlens[s+1]); out[T, nq*d]. */
-int ssb_prefill_attention(const void* qkv, int ld, int nq, int nk, int head_dim,
+/* Causal prefill over packed sequences: qkv[total_tokens, (nq+2nk)*d] (RoPE
+ * applied), sequence s spans rows [cu_seqlens[s], cu_seqlens[s+1]);
+ * out[T, nq*d].  variant 0 = auto (tcgen05/TMEM kernel for head_dim 128),
+ * 1 = the mma.sync kernel (head_dim 64 always uses it). */
+int ssb_prefill_attention(const void* qkv, int ld, int total_tokens, int nq, int nk, int head_dim,
                           const int32_t* cu_seqlens, int nseq, int max_len, void* out, int ldo,
-                          float softmax_scale, void* stream);
+                          float softmax_scale, int variant, void* stream);
 
 /* Paged GQA decode, one query token per sequence: q = qkv[b, 0:nq*d];
  * K/V of local layer `layer` read from the pool through

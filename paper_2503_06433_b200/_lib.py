@@ -68,7 +68,7 @@ SIGNATURES: dict[str, list] = {
     "ssb_embedding": [_P, _I, _P, _I, _I, _I, _P, _I, _P],
     "ssb_argmax_rows": [_P, _I, _I, _I, _I, _P, _P, _P],
     "ssb_argmax_combine": [_P, _P, _I, _I, _P, _P],
-    "ssb_prefill_attention": [_P, _I, _I, _I, _I, _P, _I, _I, _P, _I, _F, _P],
+    "ssb_prefill_attention": [_P, _I, _I, _I, _I, _I, _P, _I, _I, _P, _I, _F, _I, _P],
     "ssb_decode_attention": [_P, _I, _I, _I, _P, KVGeometry, _I, _I, _P, _I, _P, _I, _P, _I, _F, _P],
 }
 

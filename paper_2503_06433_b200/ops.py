@@ -223,13 +223,16 @@ def argmax_combine(vals: torch.Tensor, idxs: torch.Tensor, out_idx: torch.Tensor
 
 
 def prefill_attention(qkv: torch.Tensor, nq: int, nk: int, head_dim: int, cu_seqlens: torch.Tensor,
-                      max_len: int, out: torch.Tensor, scale: float) -> torch.Tensor:
+                      max_len: int, out: torch.Tensor, scale: float, variant: int = 0) -> torch.Tensor:
+    """Causal varlen attention over packed prompts (variant 0: tcgen05 kernel
+    for head_dim 128; 1: mma.sync kernel)."""
     _check(qkv, "qkv")
     _check(out, "out")
     if cu_seqlens.dtype != torch.int32:
         raise ValueError("prefill_attention: cu_seqlens must be int32")
-    call("ssb_prefill_attention", qkv.data_ptr(), qkv.stride(0), nq, nk, head_dim, cu_seqlens.data_ptr(),
-         cu_seqlens.numel() - 1, max_len, out.data_ptr(), out.stride(0), scale, _stream())
+    call("ssb_prefill_attention", qkv.data_ptr(), qkv.stride(0), qkv.shape[0], nq, nk, head_dim,
+         cu_seqlens.data_ptr(), cu_seqlens.numel() - 1, max_len, out.data_ptr(), out.stride(0), scale, variant,
+         _stream())
     return out
 
 

@@ -131,14 +131,15 @@ def _attn_ref(q, k, v, causal_offset=None):
     return torch.einsum("hqk,khd->qhd", s.softmax(-1), v)
 
 
+@pytest.mark.parametrize("variant", [0, 1])
 @pytest.mark.parametrize("d,nq,nk,lens", [(128, 8, 2, [1024, 77, 130]), (64, 4, 4, [64, 1, 200]),
-                                          (128, 32, 8, [300])])
-def test_prefill_attention(cuda, d, nq, nk, lens):
+                                          (128, 32, 8, [300]), (128, 4, 4, [128, 129, 1, 255, 256])])
+def test_prefill_attention(cuda, d, nq, nk, lens, variant):
     T = sum(lens)
     qkv = torch.randn(T, (nq + 2 * nk) * d, device=cuda).to(torch.bfloat16)
     cu = torch.tensor(np.concatenate([[0], np.cumsum(lens)]), dtype=torch.int32, device=cuda)
     out = torch.empty(T, nq * d, dtype=torch.bfloat16, device=cuda)
-    ops.prefill_attention(qkv, nq, nk, d, cu, max(lens), out, 1 / math.sqrt(d))
+    ops.prefill_attention(qkv, nq, nk, d, cu, max(lens), out, 1 / math.sqrt(d), variant=variant)
     x = qkv.float().view(T, nq + 2 * nk, d)
     start = 0
     for L in lens:

@@ -56,6 +56,20 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--what", default="gemm")
     args = ap.parse_args()
+    if args.what == "attn":
+        import numpy as np
+
+        for lens in ([1024] * 16, [1024] * 4, [4096] * 2):
+            nq, nk, d = 32, 8, 128
+            T = sum(lens)
+            qkv = torch.randn(T, (nq + 2 * nk) * d, device="cuda").to(torch.bfloat16)
+            cu = torch.tensor(np.concatenate([[0], np.cumsum(lens)]), dtype=torch.int32, device="cuda")
+            out = torch.empty(T, nq * d, dtype=torch.bfloat16, device="cuda")
+            fl = sum(2 * 2 * L * L / 2 * d * nq for L in lens)
+            for v in (0, 1):
+                ms = timed(lambda: ops.prefill_attention(qkv, nq, nk, d, cu, max(lens), out, d ** -0.5, variant=v))
+                print(json.dumps({"lens": f"{len(lens)}x{lens[0]}", "variant": v, "ms": ms,
+                                  "tflops": fl / ms / 1e9}), flush=True)
     if args.what == "mc":
         MC1, MC2 = 1 << 16, 1 << 17
         shapes = [(8192, 6144, 4096), (8192, 28672, 4096), (8192, 4096, 14336), (512, 6144, 4096),
