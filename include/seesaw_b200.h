@@ -58,6 +58,9 @@ int ssb_gemm_bf16(const void* A, const void* B, void* C, const void* R, int M, i
  * (default single CTAs, SSB_GEMM_MC1). */
 #define SSB_GEMM_MC1 (1 << 16)
 #define SSB_GEMM_MC2 (1 << 17)
+/* CTA pair issuing cta_group::2 MMAs (M = 256 per pair, B split across the
+ * pair's shared memory). */
+#define SSB_GEMM_2SM (1 << 18)
 
 /* ------------------------------------------------------------------------
  * KV re-shard between two parallelism layouts of the paged pool.

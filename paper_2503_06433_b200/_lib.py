@@ -18,6 +18,7 @@ SSB_EPI_SILU_MUL = 2
 SSB_EPI_F32 = 3
 SSB_GEMM_MC1 = 1 << 16
 SSB_GEMM_MC2 = 1 << 17
+SSB_GEMM_2SM = 1 << 18
 SSB_MAX_PEERS = 64
 
 

@@ -37,10 +37,13 @@ constexpr int kGroupM = 16;   // tile rasterisation: 16 M-tiles share a B band i
 
 constexpr int pow2_at_least(int x) { return x <= 32 ? 32 : x <= 64 ? 64 : x <= 128 ? 128 : x <= 256 ? 256 : 512; }
 
-template <int BN>
+// MODE 0: one CTA per tile.  MODE 1: CTA pair, B tile multicast (each CTA
+// still holds all BN rows of B).  MODE 2: CTA pair running cta_group::2 MMAs
+// (M = 256 per pair): each CTA holds its 128 rows of A and HALF of B.
+template <int BN, int MODE = 0>
 struct Cfg {
   static constexpr int kABytes = kBM * kBK * 2;
-  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kBBytes = (MODE == 2 ? BN / 2 : BN) * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   // as many stages as ~220 KB of shared memory holds (>= 4)
   static constexpr int kStages = (220 * 1024) / kStageBytes > 8 ? 8 : (220 * 1024) / kStageBytes;
@@ -83,11 +86,20 @@ __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x));
 // (TMA .multicast::cluster), halving B's L2->SM traffic.  A stage may be
 // refilled only when both CTAs' MMAs released it, so MMA completion is
 // committed to the empty barrier of both CTAs.
-template <int BN, int MC>
+//
+// MODE 2 (cta_group::2): the pair computes a 256 x BN tile with single-thread
+// MMAs issued by the leader CTA (M = 256 split by rows across the two CTAs'
+// TMEM, B split by columns across their smem), so each SM ingests 16 KB of A
+// and BN/2 x 128 B of B per k-block instead of 16 KB + BN x 128 B.  Both CTAs'
+// TMA loads complete on the LEADER's full barrier; the leader's commits
+// arrive on both CTAs' empty / tmem-full barriers; both epilogues release the
+// leader's tmem-empty barrier.
+template <int BN, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmap_a,
                     const __grid_constant__ CUtensorMap tmap_b, const Params p) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, MODE>;
+  constexpr int MC = MODE ? 2 : 1;
   const int crank = MC > 1 ? static_cast<int>(cluster_ctarank()) : 0;
   const int cid = blockIdx.x / MC;
   const int nclusters = gridDim.x / MC;
@@ -115,15 +127,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tmap_b);
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], MC);  // both CTAs' MMAs must release a multicast stage
+      // MODE 1: both CTAs' MMAs release a multicast stage; MODE 2: the
+      // leader's single commit arrives on both CTAs' barriers
+      mbar_init(&empty[s], MODE == 1 ? 2 : 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[s], MODE == 2 ? 8 : 4);  // one arrive per epilogue warp (of both CTAs)
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
+  if (warp == 1) {
+    if (MODE == 2)
+      tmem_alloc_cg2(tmem_slot, C::kTmemCols);
+    else
+      tmem_alloc(tmem_slot, C::kTmemCols);
+  }
   tc_fence_before();
   __syncthreads();
   if (MC > 1) cluster_sync_all();  // peer barriers initialised before any multicast lands
@@ -145,6 +164,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int tm = um * MC + crank;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
+          if (MODE == 2) {
+            // both halves land on the leader's full barrier
+            const uint32_t lbar = mapa_shared(&full[stage], 0);
+            if (crank == 0) mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
+            tma_load_2d_cg2(smem_a + stage * C::kABytes, &tmap_a, lbar, kb * kBK, tm * kBM, pol_a);
+            tma_load_2d_cg2(smem_b + stage * C::kBBytes, &tmap_b, lbar, kb * kBK, tn * BN + crank * (BN / 2),
+                            pol_b);
+            if (++stage == C::kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
           tma_load_2d(smem_a + stage * C::kABytes, &tmap_a, &full[stage], kb * kBK, tm * kBM,
                       pol_a);
@@ -164,9 +196,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
-      constexpr uint32_t idesc = idesc_bf16_f32(kBM, BN);
+    if (lane == 0 && (MODE != 2 || crank == 0)) {
+      // ---------------- MMA issuer (leader CTA only in MODE 2) ----------------
+      constexpr uint32_t idesc = idesc_bf16_f32(MODE == 2 ? 2 * kBM : kBM, BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -183,10 +215,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < kBK / kUmmaK; ++k) {
             // advance 16 elements (32 B) along K inside the 128 B swizzle row
-            umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            if (MODE == 2)
+              umma_bf16_cg2(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            else
+              umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
           }
-          // frees the smem slot (in every CTA that received multicast into it)
-          if (MC == 1)
+          // frees the smem slot (in every CTA that received data into it)
+          if (MODE == 2)
+            umma_commit_cg2_mc(&empty[stage], 0x3);
+          else if (MC == 1)
             umma_commit(&empty[stage]);
           else
             umma_commit_mc(&empty[stage], static_cast<uint16_t>((1u << MC) - 1));
@@ -195,7 +232,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        // accumulator ready for the epilogue(s)
+        if (MODE == 2)
+          umma_commit_cg2_mc(&tfull[acc], 0x3);
+        else
+          umma_commit(&tfull[acc]);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -313,7 +354,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (MODE == 2)
+          mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));  // the leader owns the accumulator pipeline
+        else
+          mbar_arrive(&tempty[acc]);
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -325,25 +371,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (MC > 1) cluster_sync_all();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, C::kTmemCols);
+    if (MODE == 2)
+      tmem_dealloc_cg2(tmem_base, C::kTmemCols);
+    else
+      tmem_dealloc(tmem_base, C::kTmemCols);
   }
 }
 
-template <int BN, int MC>
+template <int BN, int MODE>
 int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, int K, int lda,
            int ldb, int ldc, int ldr, int epi, cudaStream_t stream, int max_ctas) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, MODE>;
+  constexpr int MC = MODE ? 2 : 1;
   CUtensorMap ta, tb;
   int rc = encode_tmap_2d_bf16(&ta, A, K, M, static_cast<uint64_t>(lda) * 2, kBK, kBM);
   if (rc) return rc;
   rc = encode_tmap_2d_bf16(&tb, B, K, N, static_cast<uint64_t>(ldb) * 2, kBK, BN / MC);
   if (rc) return rc;
-  static bool attr_done = false;  // per <BN, MC> instantiation
+  static bool attr_done = false;  // per <BN, MODE> instantiation
   if (!attr_done) {
-    SSB_CUDA(cudaFuncSetAttribute(gemm_bf16_sm100<BN, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SSB_CUDA(cudaFuncSetAttribute(gemm_bf16_sm100<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   C::kSmemBytes));
-    if (MC > 1)
-      SSB_CUDA(cudaFuncSetAttribute(gemm_bf16_sm100<BN, MC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr_done = true;
   }
   Params p;
@@ -370,7 +418,7 @@ int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, 
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
   grid = std::min(grid / MC, units) * MC;
   if (MC == 1) {
-    gemm_bf16_sm100<BN, 1><<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, p);
+    gemm_bf16_sm100<BN, MODE><<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, p);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
@@ -384,7 +432,7 @@ int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    SSB_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_sm100<BN, MC>, ta, tb, p));
+    SSB_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_sm100<BN, MODE>, ta, tb, p));
   }
   return check_launch("gemm_bf16_sm100");
 }
@@ -441,13 +489,26 @@ extern "C" int ssb_gemm_bf16(const void* A, const void* B, void* C, const void* 
   // measured on B200 (tools/bench_kernels.py --what mc): B multicast across a
   // CTA pair is 2-8% SLOWER than single CTAs on the Llama shapes (L2->SM
   // bandwidth is not the limiter), so pairs are opt-in
-  int mc = (block_n & SSB_GEMM_MC2) ? 2 : 1;
-  if (bn == 0) bn = choose_bn(M, N, max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms(), epilogue);
+  int mode = (block_n & SSB_GEMM_2SM) ? 2 : (block_n & SSB_GEMM_MC2) ? 1 : 0;
+  const int sms = max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms();
+  if (bn == 0 && !(block_n & (SSB_GEMM_MC1 | SSB_GEMM_MC2 | SSB_GEMM_2SM))) {
+    // measured (tools/bench_kernels.py --what mc): cta_group::2 pairs with
+    // 256-wide tiles are 3-11% faster whenever they fill every SM pair
+    // (prefill projections, decode gate/up and LM head); narrower problems
+    // keep single-CTA tiles sized by wave efficiency
+    const long pair_units = static_cast<long>((M + 2 * kBM - 1) / (2 * kBM)) * ((N + 255) / 256);
+    if (M > kBM && pair_units >= sms / 2) {
+      mode = 2;
+      bn = 256;
+    }
+  }
+  if (bn == 0) bn = choose_bn(M, N, sms, epilogue);
   if (epilogue == SSB_EPI_SILU_MUL && bn % 64) return fail_arg("ssb_gemm_bf16: SiLU epilogue needs block_n %% 64 == 0");
-#define SSB_GEMM_CASE(BN_)                                                                              \
-  case BN_:                                                                                            \
-    return mc == 2 ? launch<BN_, 2>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas)   \
-                   : launch<BN_, 1>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas);
+#define SSB_GEMM_CASE(BN_)                                                                                       \
+  case BN_:                                                                                                     \
+    return mode == 2   ? launch<BN_, 2>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas)         \
+           : mode == 1 ? launch<BN_, 1>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas)         \
+                       : launch<BN_, 0>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas);
   switch (bn) {
     SSB_GEMM_CASE(256)
     SSB_GEMM_CASE(224)

@@ -42,19 +42,26 @@ def test_gemm_plain(cuda, M, N, K, bn):
     assert err <= tol, f"max err {err} > {tol}"
 
 
-@pytest.mark.parametrize("mc", [1, 2])
+@pytest.mark.parametrize("mode", ["mc1", "mc2", "2sm"])
 @pytest.mark.parametrize("M,N,K,bn", [(300, 640, 512, 128), (512, 4096, 1024, 192), (1000, 768, 4096, 256),
-                                      (129, 448, 256, 224), (64, 256, 128, 128)])
-def test_gemm_cluster_multicast(cuda, mc, M, N, K, bn):
-    from paper_2503_06433_b200._lib import SSB_GEMM_MC1, SSB_GEMM_MC2
+                                      (129, 448, 256, 224), (64, 256, 128, 128), (2048, 1024, 4096, 256)])
+def test_gemm_cluster_modes(cuda, mode, M, N, K, bn):
+    from paper_2503_06433_b200._lib import SSB_GEMM_2SM, SSB_GEMM_MC1, SSB_GEMM_MC2
 
+    flag = {"mc1": SSB_GEMM_MC1, "mc2": SSB_GEMM_MC2, "2sm": SSB_GEMM_2SM}[mode]
     g = torch.Generator(device="cuda").manual_seed(M + N + K)
     a = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
     w = (torch.randn(N, K, device=cuda, generator=g) / K**0.5).to(torch.bfloat16)
-    out = ops.gemm(a, w, block_n=bn | (SSB_GEMM_MC2 if mc == 2 else SSB_GEMM_MC1))
+    out = ops.gemm(a, w, block_n=bn | flag)
     torch.cuda.synchronize()
     ref = _ref(a, w)
     assert (out.float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item() + 1e-2
+    # fused epilogues through the pair path too
+    r = torch.randn(M, N, device=cuda).to(torch.bfloat16)
+    exp = ref + r.float()
+    ops.gemm(a, w, out=r, residual=r, block_n=bn | flag)
+    torch.cuda.synchronize()
+    assert (r.float() - exp).abs().max().item() <= 2e-2 * exp.abs().max().item() + 2e-2
 
 
 def test_gemm_residual_inplace(cuda):

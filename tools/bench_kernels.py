@@ -71,10 +71,11 @@ if __name__ == "__main__":
                 print(json.dumps({"lens": f"{len(lens)}x{lens[0]}", "variant": v, "ms": ms,
                                   "tflops": fl / ms / 1e9}), flush=True)
     if args.what == "mc":
-        MC1, MC2 = 1 << 16, 1 << 17
+        MC1, TWO = 1 << 16, 1 << 18
         shapes = [(8192, 6144, 4096), (8192, 28672, 4096), (8192, 4096, 14336), (512, 6144, 4096),
                   (512, 4096, 4096), (512, 28672, 4096), (512, 4096, 14336), (512, 128256, 4096)]
-        bench_gemm([(M, N, K, MC1) for M, N, K in shapes] + [(M, N, K, MC2) for M, N, K in shapes])
+        bench_gemm([(M, N, K, MC1) for M, N, K in shapes] + [(M, N, K, TWO) for M, N, K in shapes]
+                   + [(M, N, K, TWO | 256) for M, N, K in shapes[3:]])
     if args.what == "gemm":
         bench_gemm([
             (8192, 6144, 4096, 256), (8192, 4096, 4096, 256), (8192, 28672, 4096, 256),
