@@ -165,7 +165,11 @@ class Worker:
         under any (tp, pp) with the same tp*pp."""
         self.num_blocks = num_blocks
         geo = self.geometry()
-        self.pool = torch.empty(num_blocks * geo.block_elems, dtype=torch.bfloat16, device=self.device)
+        # zero-filled once: decode attention multiplies the (masked, p = 0)
+        # tail of a sequence's last block by its V rows, and never-written
+        # memory may hold NaN bit patterns (0 * NaN = NaN).  Afterwards a block
+        # only ever holds finite KV of some sequence.
+        self.pool = torch.zeros(num_blocks * geo.block_elems, dtype=torch.bfloat16, device=self.device)
 
     # ------------------------------------------------------- re-partition --
     def repartition_weights(self, cfg_new: ParallelismConfig) -> int:
