@@ -334,9 +334,10 @@ def profile_kernels(one, prompts, arch, args, dev, comm, world) -> dict:
     from paper_2503_06433_b200 import _lib
 
     def tagger(name, a):
-        if name == "ssb_gemm_bf16":
+        if name in ("ssb_gemm_bf16", "ssb_gemm_bf16_ws"):
             M, N, K = a[4], a[5], a[6]
-            return "gemm", 2.0 * M * N * K, 0
+            # decode projections run at M = resident batch; prefill at packed tokens
+            return ("gemm_prefill" if M > args.prompts else "gemm_decode"), 2.0 * M * N * K, 0
         return name.replace("ssb_", ""), 0, 0
 
     _lib.STATS.records = []
@@ -359,6 +360,12 @@ def profile_kernels(one, prompts, arch, args, dev, comm, world) -> dict:
         d["s"] += a.elapsed_time(b) / 1e3
         d["flops"] += fl
     _lib.STATS.records = []
+    g = {"launches": 0, "s": 0.0, "flops": 0.0}
+    for tag in ("gemm_prefill", "gemm_decode"):
+        for k in g:
+            g[k] += agg.get(tag, {}).get(k, 0)
+    if g["launches"]:
+        agg["gemm"] = g
     # algorithmic bytes of decode attention: every step reads ctx tokens of K and V per layer
     n = world
     kv_tok_layer = 2 * (arch.num_kv_heads // n) * arch.head_dim * 2
@@ -367,6 +374,8 @@ def profile_kernels(one, prompts, arch, args, dev, comm, world) -> dict:
     out = {"_batch_s": total}
     for tag, d in sorted(agg.items(), key=lambda kv: -kv[1]["s"]):
         r = {"launches": d["launches"], "s": d["s"], "share": d["s"] / total}
+        if tag == "gemm":
+            r["note"] = "all tcgen05 GEMM launches (= gemm_prefill + gemm_decode)"
         if d["flops"]:
             r["tflops"] = d["flops"] / d["s"] / 1e12
         if tag == "decode_attention":

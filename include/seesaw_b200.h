@@ -61,6 +61,28 @@ int ssb_gemm_bf16(const void* A, const void* B, void* C, const void* R, int M, i
 /* CTA pair issuing cta_group::2 MMAs (M = 256 per pair, B split across the
  * pair's shared memory). */
 #define SSB_GEMM_2SM (1 << 18)
+/* block_n bits 20-27: force split-K into n k-ranges (needs a workspace). */
+#define SSB_GEMM_SPLIT_SHIFT 20
+#define SSB_GEMM_SPLIT(n) ((n) << SSB_GEMM_SPLIT_SHIFT)
+
+/* The same GEMM with a split-K workspace.  With block_n = 0 the library picks
+ * (CTA pairs or single CTAs, N tile, number of k-splits) from a cost model of
+ * the persistent schedule on this GPU's SM count; it only splits K when the
+ * fp32 partials fit `workspace_bytes`.  Split tiles are reduced inside the
+ * kernel by the last-arriving warp of each tile quadrant, summing the
+ * partials in split order (deterministic).  The workspace (256-byte aligned
+ * device memory) must be ZEROED once before its first use; the kernel leaves
+ * its tile counters zero again.  One workspace per stream: concurrent GEMMs
+ * must not share it.  This is what lets the skinny decode projections
+ * (M = batch <= 512 rows, TP-sharded N or K) fill all 148 SMs. */
+int ssb_gemm_bf16_ws(const void* A, const void* B, void* C, const void* R, int M, int N, int K,
+                     int lda, int ldb, int ldc, int ldr, int epilogue, int block_n, int max_ctas,
+                     void* workspace, int64_t workspace_bytes, void* stream);
+/* The configuration block_n = 0 would pick: out_plan[3] = {mode (0 single
+ * CTA, 2 CTA pair), N tile, splits}; returns the workspace bytes it needs
+ * (0 without split-K), <0 on argument error. */
+int64_t ssb_gemm_plan(int M, int N, int K, int epilogue, int max_ctas, int64_t workspace_bytes,
+                      int32_t* out_plan);
 
 /* ------------------------------------------------------------------------
  * KV re-shard between two parallelism layouts of the paged pool.

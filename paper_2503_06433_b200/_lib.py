@@ -19,6 +19,7 @@ SSB_EPI_F32 = 3
 SSB_GEMM_MC1 = 1 << 16
 SSB_GEMM_MC2 = 1 << 17
 SSB_GEMM_2SM = 1 << 18
+SSB_GEMM_SPLIT_SHIFT = 20
 SSB_MAX_PEERS = 64
 
 
@@ -57,6 +58,7 @@ _PI64 = ctypes.POINTER(ctypes.c_int64)
 # name -> argtypes (restype is int for all compute entry points)
 SIGNATURES: dict[str, list] = {
     "ssb_gemm_bf16": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P],
+    "ssb_gemm_bf16_ws": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _I64, _P],
     "ssb_kv_reshard_pack": [_P, KVGeometry, _P, _I, _I, _PI32, _PI32, _PI32, _PI32, _PI64, _P, _P],
     "ssb_kv_reshard_unpack": [_P, KVGeometry, _P, _I, _I, _PI32, _PI32, _PI32, _PI32, _PI64, _P, _P],
     "ssb_copy2d_batched": [_P, _P, _P, _I, _I64, _P],
@@ -93,6 +95,8 @@ def load() -> ctypes.CDLL:
             lib.ssb_last_error.argtypes = []
             lib.ssb_version.restype = ctypes.c_int
             lib.ssb_device_sm_count.restype = ctypes.c_int
+            lib.ssb_gemm_plan.restype = ctypes.c_int64
+            lib.ssb_gemm_plan.argtypes = [_I, _I, _I, _I, _I, _I64, _PI32]
             for name, args in SIGNATURES.items():
                 fn = getattr(lib, name)
                 fn.argtypes = args

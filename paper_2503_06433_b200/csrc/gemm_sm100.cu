@@ -59,6 +59,12 @@ struct Params {
   int epi;
   int tiles_m, tiles_n;
   int group_n;     // rasterisation band orientation (see tile_coords)
+  // split-K: every output tile is computed as `splits` partial sums over
+  // k-block ranges of kb_per_split; the last warp to finish a tile quadrant
+  // (counter) reduces the fp32 partials in split order and runs the epilogue
+  int splits, kb_per_split;
+  float* ws;       // [tiles_m * tiles_n][splits][128][BN] fp32 partials
+  int* counters;   // [tiles_m * tiles_n][4], zero between launches (self-resetting)
 };
 
 // Grouped rasterisation: kGroupM tiles of the "band" dimension share one
@@ -79,6 +85,104 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
 }
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+// Final epilogue of 32 accumulator columns [col, col+32) of one row.
+__device__ __forceinline__ void store_cols(const Params& p, int row, int col, float (&f)[32]) {
+  __nv_bfloat16* crow = reinterpret_cast<__nv_bfloat16*>(p.C) + static_cast<size_t>(row) * p.ldc;
+  const __nv_bfloat16* rrow =
+      p.epi == SSB_EPI_RESIDUAL ? reinterpret_cast<const __nv_bfloat16*>(p.R) + static_cast<size_t>(row) * p.ldr
+                                : nullptr;
+  if (p.epi == SSB_EPI_F32) {
+    float* frow = reinterpret_cast<float*>(p.C) + static_cast<size_t>(row) * p.ldc;
+    if (col + 32 <= p.N) {
+      float4* dst = reinterpret_cast<float4*>(frow + col);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) dst[v] = make_float4(f[4 * v], f[4 * v + 1], f[4 * v + 2], f[4 * v + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col + j < p.N) frow[col + j] = f[j];
+    }
+  } else if (col + 32 <= p.N) {
+    if (rrow) {
+      const uint4* src = reinterpret_cast<const uint4*>(rrow + col);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint4 r = src[v];
+        f[8 * v + 0] += bf16_lo(r.x); f[8 * v + 1] += bf16_hi(r.x);
+        f[8 * v + 2] += bf16_lo(r.y); f[8 * v + 3] += bf16_hi(r.y);
+        f[8 * v + 4] += bf16_lo(r.z); f[8 * v + 5] += bf16_hi(r.z);
+        f[8 * v + 6] += bf16_lo(r.w); f[8 * v + 7] += bf16_hi(r.w);
+      }
+    }
+    uint4* dst = reinterpret_cast<uint4*>(crow + col);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      uint4 o;
+      o.x = pack_bf16x2(f[8 * v + 0], f[8 * v + 1]);
+      o.y = pack_bf16x2(f[8 * v + 2], f[8 * v + 3]);
+      o.z = pack_bf16x2(f[8 * v + 4], f[8 * v + 5]);
+      o.w = pack_bf16x2(f[8 * v + 6], f[8 * v + 7]);
+      dst[v] = o;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (col + j < p.N) {
+        float v = f[j];
+        if (rrow) v += __bfloat162float(rrow[col + j]);
+        crow[col + j] = __float2bfloat16_rn(v);
+      }
+    }
+  }
+}
+
+// SiLU(gate) * up of 32 (gate, up) column pairs -> output columns [col, col+32).
+__device__ __forceinline__ void store_silu(const Params& p, int row, int col, const float (&g)[32],
+                                           const float (&u)[32]) {
+  __nv_bfloat16* crow = reinterpret_cast<__nv_bfloat16*>(p.C) + static_cast<size_t>(row) * p.ldc;
+  const int ncols = p.N / 2;
+  if (col + 32 <= ncols) {
+    uint4* dst = reinterpret_cast<uint4*>(crow + col);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      uint4 o;
+      o.x = pack_bf16x2(silu(g[8 * v + 0]) * u[8 * v + 0], silu(g[8 * v + 1]) * u[8 * v + 1]);
+      o.y = pack_bf16x2(silu(g[8 * v + 2]) * u[8 * v + 2], silu(g[8 * v + 3]) * u[8 * v + 3]);
+      o.z = pack_bf16x2(silu(g[8 * v + 4]) * u[8 * v + 4], silu(g[8 * v + 5]) * u[8 * v + 5]);
+      o.w = pack_bf16x2(silu(g[8 * v + 6]) * u[8 * v + 6], silu(g[8 * v + 7]) * u[8 * v + 7]);
+      dst[v] = o;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (col + j < ncols) crow[col + j] = __float2bfloat16_rn(silu(g[j]) * u[j]);
+  }
+}
+
+// Split-K partial layout, per (tile, split): [BN/4 float4 columns][128 rows]
+// of float4, so one warp's store or load of a column group covers 512
+// contiguous bytes (32 rows).  Sum of the `splits` partials of 32 columns
+// (8 float4 groups starting at column group g0) in split order: bitwise
+// independent of which split finished last.
+__device__ __forceinline__ void sum_partials(const float4* base, size_t split_stride4, int splits, int g0,
+                                             float (&f)[32]) {
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    const float4 x = __ldcg(base + (g0 + v) * kBM);
+    f[4 * v] = x.x; f[4 * v + 1] = x.y; f[4 * v + 2] = x.z; f[4 * v + 3] = x.w;
+  }
+  for (int s = 1; s < splits; ++s) {
+    const float4* src = base + s * split_stride4;
+    float4 x[8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) x[v] = __ldcg(src + (g0 + v) * kBM);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      f[4 * v] += x[v].x; f[4 * v + 1] += x[v].y; f[4 * v + 2] += x[v].z; f[4 * v + 3] += x[v].w;
+    }
+  }
+}
 
 // MC = CTAs per cluster along M.  With MC = 2 the two CTAs of a cluster
 // compute vertically adjacent M tiles of the same N tile: each loads its own
@@ -119,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int num_units = units_m * p.tiles_n;
+  const int num_units = units_m * p.tiles_n * p.splits;
   const int num_kb = (p.K + kBK - 1) / kBK;
 
   if (warp == 0 && lane == 0) {
@@ -160,9 +264,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int u = cid; u < num_units; u += nclusters) {
         int um, tn;
-        tile_coords(u, units_m, p.tiles_n, p.group_n, um, tn);
+        tile_coords(u / p.splits, units_m, p.tiles_n, p.group_n, um, tn);
         const int tm = um * MC + crank;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int kb0 = (u % p.splits) * p.kb_per_split;
+        const int kb1 = min(num_kb, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (MODE == 2) {
             // both halves land on the leader's full barrier
@@ -207,7 +313,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int kb0 = (u % p.splits) * p.kb_per_split;
+        const int kb1 = min(num_kb, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t adesc = sdesc_k_sw128(smem_u32(smem_a + stage * C::kABytes));
@@ -216,9 +324,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < kBK / kUmmaK; ++k) {
             // advance 16 elements (32 B) along K inside the 128 B swizzle row
             if (MODE == 2)
-              umma_bf16_cg2(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+              umma_bf16_cg2(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb != kb0) || (k != 0));
             else
-              umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+              umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb != kb0) || (k != 0));
           }
           // frees the smem slot (in every CTA that received data into it)
           if (MODE == 2)
@@ -248,117 +356,105 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     for (int u = cid; u < num_units; u += nclusters) {
       int um, tn;
-      tile_coords(u, units_m, p.tiles_n, p.group_n, um, tn);
+      const int t = u / p.splits;
+      tile_coords(t, units_m, p.tiles_n, p.group_n, um, tn);
       const int tm = um * MC + crank;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = tm * kBM + q * 32 + lane;
       const bool row_ok = row < p.M;
       const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      __nv_bfloat16* crow = reinterpret_cast<__nv_bfloat16*>(p.C) + static_cast<size_t>(row) * p.ldc;
-      if (p.epi == SSB_EPI_SILU_MUL) {
-        // accumulator columns come in (32 gate, 32 up) pairs -> 32 outputs
+      if (p.splits == 1) {
+        if (p.epi == SSB_EPI_SILU_MUL) {
+          // accumulator columns come in (32 gate, 32 up) pairs -> 32 outputs
 #pragma unroll 1
-        for (int c = 0; c < BN / 64; ++c) {
-          uint32_t g[32], u[32];
-          tmem_ld32(tbase + c * 64, g);
-          tmem_ld32(tbase + c * 64 + 32, u);
-          tmem_ld_wait();
-          const int col = (tn * BN) / 2 + c * 32;
-          const int ncols = p.N / 2;
-          if (row_ok) {
-            if (col + 32 <= ncols) {
-              uint4* dst = reinterpret_cast<uint4*>(crow + col);
+          for (int c = 0; c < BN / 64; ++c) {
+            uint32_t g[32], v[32];
+            tmem_ld32(tbase + c * 64, g);
+            tmem_ld32(tbase + c * 64 + 32, v);
+            tmem_ld_wait();
+            float gf[32], uf[32];
 #pragma unroll
-              for (int v = 0; v < 4; ++v) {
-                uint4 o;
-                o.x = pack_bf16x2(silu(__uint_as_float(g[8 * v + 0])) * __uint_as_float(u[8 * v + 0]),
-                                  silu(__uint_as_float(g[8 * v + 1])) * __uint_as_float(u[8 * v + 1]));
-                o.y = pack_bf16x2(silu(__uint_as_float(g[8 * v + 2])) * __uint_as_float(u[8 * v + 2]),
-                                  silu(__uint_as_float(g[8 * v + 3])) * __uint_as_float(u[8 * v + 3]));
-                o.z = pack_bf16x2(silu(__uint_as_float(g[8 * v + 4])) * __uint_as_float(u[8 * v + 4]),
-                                  silu(__uint_as_float(g[8 * v + 5])) * __uint_as_float(u[8 * v + 5]));
-                o.w = pack_bf16x2(silu(__uint_as_float(g[8 * v + 6])) * __uint_as_float(u[8 * v + 6]),
-                                  silu(__uint_as_float(g[8 * v + 7])) * __uint_as_float(u[8 * v + 7]));
-                dst[v] = o;
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (col + j < ncols)
-                  crow[col + j] = __float2bfloat16_rn(silu(__uint_as_float(g[j])) * __uint_as_float(u[j]));
+            for (int j = 0; j < 32; ++j) {
+              gf[j] = __uint_as_float(g[j]);
+              uf[j] = __uint_as_float(v[j]);
             }
+            if (row_ok) store_silu(p, row, (tn * BN) / 2 + c * 32, gf, uf);
+          }
+        } else {
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t a[32];
+            tmem_ld32(tbase + c * 32, a);
+            tmem_ld_wait();
+            float f[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(a[j]);
+            if (row_ok) store_cols(p, row, tn * BN + c * 32, f);
           }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (MODE == 2)
+            mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));  // the leader owns the accumulator pipeline
+          else
+            mbar_arrive(&tempty[acc]);
+        }
       } else {
-        const __nv_bfloat16* rrow =
-            p.epi == SSB_EPI_RESIDUAL
-                ? reinterpret_cast<const __nv_bfloat16*>(p.R) + static_cast<size_t>(row) * p.ldr
-                : nullptr;
+        // split-K: spill this split's fp32 partial, release TMEM, and let the
+        // last of the tile quadrant's `splits` warps reduce + run the epilogue
+        const int tile = tm * p.tiles_n + tn;
+        const int split = u % p.splits;
+        const size_t split_stride4 = static_cast<size_t>(kBM) * BN / 4;  // float4 per (tile, split)
+        float4* wbase = reinterpret_cast<float4*>(p.ws) +
+                        (static_cast<size_t>(tile) * p.splits + split) * split_stride4 + q * 32 + lane;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           uint32_t a[32];
           tmem_ld32(tbase + c * 32, a);
           tmem_ld_wait();
-          const int col = tn * BN + c * 32;
-          if (row_ok) {
-            float f[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(a[j]);
-            if (p.epi == SSB_EPI_F32) {
-              float* frow = reinterpret_cast<float*>(p.C) + static_cast<size_t>(row) * p.ldc;
-              if (col + 32 <= p.N) {
-                float4* dst = reinterpret_cast<float4*>(frow + col);
-#pragma unroll
-                for (int v = 0; v < 8; ++v)
-                  dst[v] = make_float4(f[4 * v], f[4 * v + 1], f[4 * v + 2], f[4 * v + 3]);
-              } else {
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                  if (col + j < p.N) frow[col + j] = f[j];
-              }
-            } else if (col + 32 <= p.N) {
-              if (rrow) {
-                const uint4* src = reinterpret_cast<const uint4*>(rrow + col);
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                  uint4 r = src[v];
-                  f[8 * v + 0] += bf16_lo(r.x); f[8 * v + 1] += bf16_hi(r.x);
-                  f[8 * v + 2] += bf16_lo(r.y); f[8 * v + 3] += bf16_hi(r.y);
-                  f[8 * v + 4] += bf16_lo(r.z); f[8 * v + 5] += bf16_hi(r.z);
-                  f[8 * v + 6] += bf16_lo(r.w); f[8 * v + 7] += bf16_hi(r.w);
-                }
-              }
-              uint4* dst = reinterpret_cast<uint4*>(crow + col);
-#pragma unroll
-              for (int v = 0; v < 4; ++v) {
-                uint4 o;
-                o.x = pack_bf16x2(f[8 * v + 0], f[8 * v + 1]);
-                o.y = pack_bf16x2(f[8 * v + 2], f[8 * v + 3]);
-                o.z = pack_bf16x2(f[8 * v + 4], f[8 * v + 5]);
-                o.w = pack_bf16x2(f[8 * v + 6], f[8 * v + 7]);
-                dst[v] = o;
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                if (col + j < p.N) {
-                  float v = f[j];
-                  if (rrow) v += __bfloat162float(rrow[col + j]);
-                  crow[col + j] = __float2bfloat16_rn(v);
-                }
-              }
+          for (int v = 0; v < 8; ++v)
+            __stcg(wbase + (c * 8 + v) * kBM,
+                   make_float4(__uint_as_float(a[4 * v]), __uint_as_float(a[4 * v + 1]),
+                               __uint_as_float(a[4 * v + 2]), __uint_as_float(a[4 * v + 3])));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (MODE == 2)
+            mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
+          else
+            mbar_arrive(&tempty[acc]);
+        }
+        __threadfence();
+        __syncwarp();
+        int prev = 0;
+        if (lane == 0) prev = atomicAdd(&p.counters[tile * 4 + q], 1);
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev == p.splits - 1) {
+          __threadfence();
+          if (lane == 0) p.counters[tile * 4 + q] = 0;  // every split arrived: reset for the next launch
+          const float4* rbase = reinterpret_cast<const float4*>(p.ws) +
+                                static_cast<size_t>(tile) * p.splits * split_stride4 + q * 32 + lane;
+          if (p.epi == SSB_EPI_SILU_MUL) {
+#pragma unroll 1
+            for (int c = 0; c < BN / 64; ++c) {
+              float g[32], v[32];
+              sum_partials(rbase, split_stride4, p.splits, c * 16, g);
+              sum_partials(rbase, split_stride4, p.splits, c * 16 + 8, v);
+              if (row_ok) store_silu(p, row, (tn * BN) / 2 + c * 32, g, v);
+            }
+          } else {
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+              float f[32];
+              sum_partials(rbase, split_stride4, p.splits, c * 8, f);
+              if (row_ok) store_cols(p, row, tn * BN + c * 32, f);
             }
           }
         }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (MODE == 2)
-          mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));  // the leader owns the accumulator pipeline
-        else
-          mbar_arrive(&tempty[acc]);
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
@@ -380,7 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int BN, int MODE>
 int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, int K, int lda,
-           int ldb, int ldc, int ldr, int epi, cudaStream_t stream, int max_ctas) {
+           int ldb, int ldc, int ldr, int epi, cudaStream_t stream, int max_ctas, int splits, void* ws) {
   using C = Cfg<BN, MODE>;
   constexpr int MC = MODE ? 2 : 1;
   CUtensorMap ta, tb;
@@ -405,6 +501,17 @@ int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, 
   p.epi = epi;
   p.tiles_m = (M + kBM - 1) / kBM;
   p.tiles_n = (N + BN - 1) / BN;
+  const int num_kb = (K + kBK - 1) / kBK;
+  p.kb_per_split = (num_kb + splits - 1) / splits;
+  p.splits = (num_kb + p.kb_per_split - 1) / p.kb_per_split;  // no empty split
+  p.counters = static_cast<int*>(ws);
+  p.ws = nullptr;
+  if (p.splits > 1) {
+    // a pair's second CTA may own a phantom M tile past the end (tiles_m odd)
+    const size_t tiles_alloc = static_cast<size_t>((p.tiles_m + MC - 1) / MC * MC) * p.tiles_n;
+    const size_t cnt_bytes = (tiles_alloc * 4 * sizeof(int) + 255) & ~size_t(255);
+    p.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + cnt_bytes);
+  }
   // band the operand whose re-streaming would cost more DRAM traffic:
   // M-bands re-read B once per band, N-bands re-read A once per band
   {
@@ -413,10 +520,10 @@ int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, 
     const double n_band = b_bytes + a_bytes * ((p.tiles_n + kGroupM - 1) / kGroupM);
     p.group_n = n_band < m_band ? 1 : 0;
   }
-  const int units = ((p.tiles_m + MC - 1) / MC) * p.tiles_n;
+  const long units = static_cast<long>((p.tiles_m + MC - 1) / MC) * p.tiles_n * p.splits;
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
-  grid = std::min(grid / MC, units) * MC;
+  grid = static_cast<int>(std::min<long>(grid / MC, units)) * MC;
   if (MC == 1) {
     gemm_bf16_sm100<BN, MODE><<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, p);
   } else {
@@ -437,25 +544,67 @@ int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, 
   return check_launch("gemm_bf16_sm100");
 }
 
-// Pick the N tile maximising wave efficiency (tiles / (waves * SMs)),
-// weighted by the per-tile efficiency of wider tiles (A-tile reuse).
-int choose_bn(int M, int N, int sms, int epi) {
+struct Plan {
+  int mode, bn, splits;
+};
+
+size_t plan_ws_bytes(int M, int N, const Plan& pl) {
+  if (pl.splits <= 1) return 0;
+  const int MC = pl.mode ? 2 : 1;
+  const size_t tiles = static_cast<size_t>(((M + kBM * MC - 1) / (kBM * MC)) * MC) * ((N + pl.bn - 1) / pl.bn);
+  return ((tiles * 4 * sizeof(int) + 255) & ~size_t(255)) + tiles * pl.splits * kBM * pl.bn * sizeof(float);
+}
+
+// Modelled time (microseconds) of one configuration: a fixed launch /
+// prologue / drain cost, rounds of persistent units (the last, partial round
+// weighted by its fill) each running its k-blocks at a per-(mode, tile)
+// k-block time, and for split-K a fixed cost plus the fp32 partial round trip.
+// The per-k-block times are not the MMA rate: at these tile shapes an SM is
+// bound by operand ingest from L2 (~64 B/clk), so wide single-CTA tiles lose
+// to CTA pairs that split B.  Constants fitted on B200 to the sweep of
+// tools/bench_kernels.py --what splitk (Llama decode shapes at M = 256/512,
+// TP1 and TP8, and prefill shapes); the fitted plan is within 1.2x of the
+// best forced configuration on every swept shape (profiles/ summary).
+double plan_cost(int M, int N, int K, int sms, const Plan& pl) {
+  const int MC = pl.mode ? 2 : 1;
   const int tm = (M + kBM - 1) / kBM;
-  const int cands[4] = {256, 224, 192, 128};
-  const double weight[4] = {1.0, 0.985, 0.97, 0.93};
-  int best = 256;
-  double best_score = -1.0;
-  for (int i = 0; i < 4; ++i) {
-    const int bn = cands[i];
-    if (epi == SSB_EPI_SILU_MUL && bn % 64) continue;  // gate/up pairs of 32 columns
-    const long tiles = static_cast<long>(tm) * ((N + bn - 1) / bn);
-    const long waves = (tiles + sms - 1) / sms;
-    // columns past N are wasted MMA work
-    const double fill = static_cast<double>(N) / (static_cast<double>((N + bn - 1) / bn) * bn);
-    const double score = static_cast<double>(tiles) / (waves * sms) * weight[i] * fill;
-    if (score > best_score + 1e-9) {
-      best_score = score;
-      best = bn;
+  const int kb = (K + kBK - 1) / kBK;
+  const int kbs = (kb + pl.splits - 1) / pl.splits;
+  const int splits = (kb + kbs - 1) / kbs;
+  const long units = static_cast<long>((tm + MC - 1) / MC) * ((N + pl.bn - 1) / pl.bn) * splits;
+  const long groups = std::max(1, sms / MC);
+  const long full = units / groups, rem = units % groups;
+  const double last_w = 0.1553;
+  const double rounds = full + (rem ? last_w * rem / groups + (1.0 - last_w) : 0.0);
+  double kb_us;
+  if (pl.mode == 2)
+    kb_us = pl.bn >= 256 ? 0.3839 : pl.bn >= 224 ? 0.3282 : pl.bn >= 192 ? 0.425 : pl.bn >= 128 ? 0.2417 : 1.0;
+  else
+    kb_us = pl.bn >= 256 ? 2.4031 : pl.bn >= 224 ? 1.435 : pl.bn >= 192 ? 0.3997 : pl.bn >= 128 ? 0.2308 : 1.0;
+  double t = 10.86 + rounds * kbs * kb_us;
+  if (splits > 1) t += 8.19 + 0.03 * static_cast<double>(units) * kBM * pl.bn * 4.0 / 1e6;
+  return t;
+}
+
+Plan choose_plan(int M, int N, int K, int epi, int sms, size_t ws_bytes) {
+  Plan best{0, 256, 1};
+  double best_t = 1e30;
+  const int bns[4] = {256, 224, 192, 128};
+  const int kb = (K + kBK - 1) / kBK;
+  for (int mode = 0; mode <= 2; mode += 2) {
+    if (mode == 2 && M <= kBM) continue;
+    for (int bn : bns) {
+      if (epi == SSB_EPI_SILU_MUL && bn % 64) continue;  // gate/up pairs of 32 columns
+      for (int sp = 1; sp <= 16; ++sp) {
+        if (sp > 1 && (kb / sp < 4)) break;
+        Plan pl{mode, bn, sp};
+        if (sp > 1 && plan_ws_bytes(M, N, pl) > ws_bytes) break;
+        const double t = plan_cost(M, N, K, sms, pl);
+        if (t < best_t * 0.995) {
+          best_t = t;
+          best = pl;
+        }
+      }
     }
   }
   return best;
@@ -464,9 +613,10 @@ int choose_bn(int M, int N, int sms, int epi) {
 }  // namespace
 }  // namespace ssb
 
-extern "C" int ssb_gemm_bf16(const void* A, const void* B, void* C, const void* R, int M, int N,
-                             int K, int lda, int ldb, int ldc, int ldr, int epilogue, int block_n,
-                             int max_ctas, void* stream) {
+namespace {
+int gemm_entry(const void* A, const void* B, void* C, const void* R, int M, int N, int K, int lda, int ldb,
+               int ldc, int ldr, int epilogue, int block_n, int max_ctas, void* workspace, int64_t ws_bytes,
+               void* stream) {
   using namespace ssb;
   SSB_REQUIRE(M > 0 && N > 0 && K > 0, "ssb_gemm_bf16: empty problem M=%d N=%d K=%d", M, N, K);
   SSB_REQUIRE(A && B && C, "ssb_gemm_bf16: null operand");
@@ -476,46 +626,77 @@ extern "C" int ssb_gemm_bf16(const void* A, const void* B, void* C, const void* 
   SSB_REQUIRE(lda >= K && ldb >= K, "ssb_gemm_bf16: lda/ldb smaller than K");
   SSB_REQUIRE(epilogue == SSB_EPI_SILU_MUL ? (N % 64 == 0 && ldc >= N / 2) : ldc >= N,
               "ssb_gemm_bf16: bad ldc/N for epilogue");
+  SSB_REQUIRE(ws_bytes >= 0 && (ws_bytes == 0 || workspace), "ssb_gemm_bf16: bad workspace");
   if (!aligned16(A) || !aligned16(B) || (lda % 8) || (ldb % 8) || !aligned16(C) ||
-      (ldc % (epilogue == SSB_EPI_F32 ? 4 : 8)) ||
-      (R && (!aligned16(R) || (ldr % 8)))) {
-    set_error("ssb_gemm_bf16: operands must be 16-byte aligned with leading dims %% 8 == 0");
+      (ldc % (epilogue == SSB_EPI_F32 ? 4 : 8)) || (R && (!aligned16(R) || (ldr % 8))) ||
+      (workspace && (reinterpret_cast<uintptr_t>(workspace) & 255))) {
+    set_error("ssb_gemm_bf16: operands must be 16-byte aligned with leading dims %% 8 == 0 "
+              "(workspace 256-byte aligned)");
     return SSB_EALIGN;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  // block_n: bits 0-15 tile width (0 = auto); SSB_GEMM_MC1 / SSB_GEMM_MC2
-  // force the cluster size (default: pairs whenever there are >= 2 M tiles)
-  int bn = block_n & 0xFFFF;
-  // measured on B200 (tools/bench_kernels.py --what mc): B multicast across a
-  // CTA pair is 2-8% SLOWER than single CTAs on the Llama shapes (L2->SM
-  // bandwidth is not the limiter), so pairs are opt-in
-  int mode = (block_n & SSB_GEMM_2SM) ? 2 : (block_n & SSB_GEMM_MC2) ? 1 : 0;
   const int sms = max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms();
-  if (bn == 0 && !(block_n & (SSB_GEMM_MC1 | SSB_GEMM_MC2 | SSB_GEMM_2SM))) {
-    // measured (tools/bench_kernels.py --what mc): cta_group::2 pairs with
-    // 256-wide tiles are 3-11% faster whenever they fill every SM pair
-    // (prefill projections, decode gate/up and LM head); narrower problems
-    // keep single-CTA tiles sized by wave efficiency
-    const long pair_units = static_cast<long>((M + 2 * kBM - 1) / (2 * kBM)) * ((N + 255) / 256);
-    if (M > kBM && pair_units >= sms / 2) {
-      mode = 2;
-      bn = 256;
-    }
+  Plan pl{0, block_n & 0xFFFF, 1};
+  const int forced_split = (block_n >> SSB_GEMM_SPLIT_SHIFT) & 0xFF;
+  if (pl.bn == 0 && !(block_n & (SSB_GEMM_MC1 | SSB_GEMM_MC2 | SSB_GEMM_2SM)) && forced_split == 0) {
+    pl = choose_plan(M, N, K, epilogue, sms, static_cast<size_t>(ws_bytes));
+  } else {
+    pl.mode = (block_n & SSB_GEMM_2SM) ? 2 : (block_n & SSB_GEMM_MC2) ? 1 : 0;
+    if (pl.bn == 0) pl.bn = 256;
+    pl.splits = forced_split ? forced_split : 1;
+    if (pl.mode == 2 && M <= kBM) pl.mode = 0;
   }
-  if (bn == 0) bn = choose_bn(M, N, sms, epilogue);
-  if (epilogue == SSB_EPI_SILU_MUL && bn % 64) return fail_arg("ssb_gemm_bf16: SiLU epilogue needs block_n %% 64 == 0");
-#define SSB_GEMM_CASE(BN_)                                                                                       \
-  case BN_:                                                                                                     \
-    return mode == 2   ? launch<BN_, 2>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas)         \
-           : mode == 1 ? launch<BN_, 1>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas)         \
-                       : launch<BN_, 0>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas);
-  switch (bn) {
+  if (epilogue == SSB_EPI_SILU_MUL && pl.bn % 64)
+    return fail_arg("ssb_gemm_bf16: SiLU epilogue needs block_n %% 64 == 0");
+  if (pl.splits > 1) {  // effective split count: no empty k-range
+    const int kb = (K + kBK - 1) / kBK, kbs = (kb + pl.splits - 1) / pl.splits;
+    pl.splits = (kb + kbs - 1) / kbs;
+  }
+  if (pl.splits > 1 && plan_ws_bytes(M, N, pl) > static_cast<size_t>(ws_bytes))
+    return fail_arg("ssb_gemm_bf16: split-K x%d needs %zu workspace bytes, have %lld", pl.splits,
+                    plan_ws_bytes(M, N, pl), static_cast<long long>(ws_bytes));
+#define SSB_GEMM_CASE(BN_)                                                                              \
+  case BN_:                                                                                            \
+    return pl.mode == 2   ? launch<BN_, 2>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas, \
+                                           pl.splits, workspace)                                       \
+           : pl.mode == 1 ? launch<BN_, 1>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas, \
+                                           pl.splits, workspace)                                       \
+                          : launch<BN_, 0>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas, \
+                                           pl.splits, workspace);
+  switch (pl.bn) {
     SSB_GEMM_CASE(256)
     SSB_GEMM_CASE(224)
     SSB_GEMM_CASE(192)
     SSB_GEMM_CASE(128)
     SSB_GEMM_CASE(64)
-    default: return fail_arg("ssb_gemm_bf16: block_n must be 0, 64, 128, 192, 224 or 256 (got %d)", bn);
+    default: return fail_arg("ssb_gemm_bf16: block_n must be 0, 64, 128, 192, 224 or 256 (got %d)", pl.bn);
   }
 #undef SSB_GEMM_CASE
+}
+}  // namespace
+
+extern "C" int ssb_gemm_bf16(const void* A, const void* B, void* C, const void* R, int M, int N, int K, int lda,
+                             int ldb, int ldc, int ldr, int epilogue, int block_n, int max_ctas, void* stream) {
+  return gemm_entry(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, block_n, max_ctas, nullptr, 0, stream);
+}
+
+extern "C" int ssb_gemm_bf16_ws(const void* A, const void* B, void* C, const void* R, int M, int N, int K,
+                                int lda, int ldb, int ldc, int ldr, int epilogue, int block_n, int max_ctas,
+                                void* workspace, int64_t workspace_bytes, void* stream) {
+  return gemm_entry(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, block_n, max_ctas, workspace,
+                    workspace_bytes, stream);
+}
+
+extern "C" int64_t ssb_gemm_plan(int M, int N, int K, int epilogue, int max_ctas, int64_t workspace_bytes,
+                                 int32_t* out_plan) {
+  using namespace ssb;
+  if (M <= 0 || N <= 0 || K <= 0) return fail_arg("ssb_gemm_plan: empty problem");
+  const int sms = max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms();
+  const Plan pl = choose_plan(M, N, K, epilogue, sms, static_cast<size_t>(std::max<int64_t>(workspace_bytes, 0)));
+  if (out_plan) {
+    out_plan[0] = pl.mode;
+    out_plan[1] = pl.bn;
+    out_plan[2] = pl.splits;
+  }
+  return static_cast<int64_t>(plan_ws_bytes(M, N, pl));
 }

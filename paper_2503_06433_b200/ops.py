@@ -12,7 +12,17 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import SSB_EPI_F32, SSB_EPI_NONE, SSB_EPI_RESIDUAL, SSB_EPI_SILU_MUL, call
+from ._lib import SSB_EPI_F32, SSB_EPI_NONE, SSB_EPI_RESIDUAL, SSB_EPI_SILU_MUL, call, load
+
+
+def gemm_plan(M: int, N: int, K: int, epilogue: int = SSB_EPI_NONE, max_ctas: int = 0,
+              workspace_bytes: int = 0) -> tuple[tuple[int, int, int], int]:
+    """((mode, block_n, splits), workspace bytes) the library picks for a shape."""
+    out = (ctypes.c_int32 * 3)()
+    need = load().ssb_gemm_plan(M, N, K, epilogue, max_ctas, workspace_bytes, out)
+    if need < 0:
+        raise ValueError(load().ssb_last_error().decode())
+    return (out[0], out[1], out[2]), int(need)
 
 
 def _stream() -> int:
@@ -35,11 +45,14 @@ def gemm(
     block_n: int = 0,
     out_f32: bool = False,
     max_ctas: int = 0,
+    workspace: torch.Tensor | None = None,
 ) -> torch.Tensor:
     """out = a @ w.T (+ residual) or silu-mul of interleaved gate/up columns,
     or fp32 output (logits) with ``out_f32``.
 
     a: [M, K] bf16 (row stride may exceed K), w: [N, K] bf16 weight.
+    workspace: zero-initialised device buffer (one per stream) that lets the
+    library split K across CTAs for skinny problems (decode projections).
     """
     _check(a, "a")
     _check(w, "w")
@@ -61,7 +74,7 @@ def gemm(
     if residual is not None:
         _check(residual, "residual")
     call(
-        "ssb_gemm_bf16",
+        "ssb_gemm_bf16_ws",
         a.data_ptr(),
         w.data_ptr(),
         out.data_ptr(),
@@ -76,6 +89,8 @@ def gemm(
         epi,
         block_n,
         max_ctas,
+        workspace.data_ptr() if workspace is not None else None,
+        workspace.numel() * workspace.element_size() if workspace is not None else 0,
         _stream(),
     )
     return out

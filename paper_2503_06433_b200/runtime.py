@@ -85,6 +85,8 @@ class LayoutState:
 class Worker:
     """One GPU of the fleet (SPMD)."""
 
+    GEMM_WS_BYTES = 64 << 20
+
     def __init__(self, arch: LlamaArch, world: Comm, dp: int, device: torch.device, seed: int = 0,
                  block_size: int = 64, max_pos: int = 4096) -> None:
         self.arch = arch
@@ -300,14 +302,15 @@ class Worker:
         eps = self.arch.rms_eps
         p = f"L{layer}."
         lead = st.rank == 0
+        ws = buf["ws"]
         h = ops.rmsnorm(x, self.w(p + "attn_norm"), eps, out=buf["h"])
-        qkv = ops.gemm(h, self.w(p + "wqkv"), out=buf["qkv"], max_ctas=cap)
+        qkv = ops.gemm(h, self.w(p + "wqkv"), out=buf["qkv"], max_ctas=cap, workspace=ws)
         attn = attn_fn(qkv, layer - st.weights.layer_begin)
-        ops.gemm(attn, self.w(p + "wo"), out=x, residual=x if lead else None, max_ctas=cap)
+        ops.gemm(attn, self.w(p + "wo"), out=x, residual=x if lead else None, max_ctas=cap, workspace=ws)
         self._reduce_into(x)
         h = ops.rmsnorm(x, self.w(p + "mlp_norm"), eps, out=buf["h"])
-        act = ops.gemm(h, self.w(p + "w13"), out=buf["act"], silu_mul=True, max_ctas=cap)
-        ops.gemm(act, self.w(p + "w2"), out=x, residual=x if lead else None, max_ctas=cap)
+        act = ops.gemm(h, self.w(p + "w13"), out=buf["act"], silu_mul=True, max_ctas=cap, workspace=ws)
+        ops.gemm(act, self.w(p + "w2"), out=x, residual=x if lead else None, max_ctas=cap, workspace=ws)
         self._reduce_into(x)
 
     def _reduce_into(self, x: torch.Tensor) -> None:
@@ -332,13 +335,18 @@ class Worker:
                 "attn": torch.empty(T, nq * a.head_dim, dtype=torch.bfloat16, device=dev),
                 "act": torch.empty(T, st.weights.ffn_local, dtype=torch.bfloat16, device=dev),
             }
+        if "ws" not in slot:
+            # split-K workspace of this lane's stream (zeroed once; the GEMM
+            # leaves its tile counters zero), see ssb_gemm_bf16_ws
+            slot["ws"] = torch.zeros(self.GEMM_WS_BYTES, dtype=torch.uint8, device=self.device)
+        slot["buf"]["ws"] = slot["ws"]
         return slot["buf"]
 
-    def _logits_argmax(self, h_last: torch.Tensor, out_tokens: torch.Tensor) -> None:
+    def _logits_argmax(self, h_last: torch.Tensor, out_tokens: torch.Tensor, ws: torch.Tensor | None = None) -> None:
         """Vocab-parallel LM head + greedy argmax (fp32 logits)."""
         st = self.state
         n = h_last.shape[0]
-        logits = ops.gemm(h_last, self.w("head"), out_f32=True)
+        logits = ops.gemm(h_last, self.w("head"), out_f32=True, workspace=ws)
         vals = torch.empty(n, dtype=torch.float32, device=self.device)
         idxs = torch.empty(n, dtype=torch.int32, device=self.device)
         ops.argmax_rows(logits, st.weights.vocab_begin, vals, idxs)
@@ -466,6 +474,6 @@ class Worker:
         for s, x, _, buf, v in lanes:
             with torch.cuda.stream(s):
                 h = ops.rmsnorm(x, self.w("final_norm"), a.rms_eps, out=buf["h"])
-                self._logits_argmax(h, v["out"])
+                self._logits_argmax(h, v["out"], buf["ws"])
         if len(spans) > 1:
             main.wait_stream(self._side)

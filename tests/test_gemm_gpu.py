@@ -100,3 +100,70 @@ def test_gemm_strided_a(cuda):
     out = ops.gemm(a, w)
     torch.cuda.synchronize()
     assert (out.float() - _ref(a, w)).abs().max().item() < 5e-2
+
+
+def _ws(cuda, nbytes=64 << 20):
+    return torch.zeros(nbytes, dtype=torch.uint8, device=cuda)
+
+
+@pytest.mark.parametrize("mode", ["single", "2sm"])
+@pytest.mark.parametrize("splits", [2, 3, 5, 16])
+@pytest.mark.parametrize("M,N,K,bn", [(512, 768, 4096, 256), (512, 4096, 512, 128), (300, 640, 1000, 192),
+                                      (129, 448, 2048, 224), (64, 256, 4096, 128)])
+def test_gemm_split_k(cuda, mode, splits, M, N, K, bn):
+    """Split-K (forced): fp32 partials reduced in-kernel by the last warp of
+    each tile quadrant; every epilogue; deterministic run to run."""
+    from paper_2503_06433_b200._lib import SSB_GEMM_2SM, SSB_GEMM_SPLIT_SHIFT
+
+    flag = bn | (splits << SSB_GEMM_SPLIT_SHIFT) | (SSB_GEMM_2SM if mode == "2sm" else 0)
+    g = torch.Generator(device="cuda").manual_seed(M + N + K + splits)
+    a = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=cuda, generator=g) / K**0.5).to(torch.bfloat16)
+    ws = _ws(cuda, 160 << 20)
+    out = ops.gemm(a, w, block_n=flag, workspace=ws)
+    out2 = ops.gemm(a, w, block_n=flag, workspace=ws)
+    torch.cuda.synchronize()
+    ref = _ref(a, w)
+    assert (out.float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item() + 1e-2
+    assert torch.equal(out, out2), "split-K reduction must be deterministic"
+    # tile counters (the workspace head) left zero: self-resetting
+    mc = 2 if (mode == "2sm" and M > 128) else 1
+    tiles = -(-M // (128 * mc)) * mc * -(-N // bn)
+    head = (tiles * 16 + 255) // 256 * 256
+    assert int(ws[:head].view(torch.int32).abs().sum()) == 0
+    r = torch.randn(M, N, device=cuda, generator=g).to(torch.bfloat16)
+    exp = ref + r.float()
+    ops.gemm(a, w, out=r, residual=r, block_n=flag, workspace=ws)
+    f = ops.gemm(a, w, out_f32=True, block_n=flag, workspace=ws)
+    torch.cuda.synchronize()
+    assert (r.float() - exp).abs().max().item() <= 2e-2 * exp.abs().max().item() + 2e-2
+    assert (f - ref).abs().max().item() <= 1e-3 * ref.abs().max().item() + 1e-3
+    if bn % 64 == 0 and N % 64 == 0:
+        F = N // 2
+        s = ops.gemm(a, w, silu_mul=True, block_n=flag, workspace=ws)
+        torch.cuda.synchronize()
+        wv = w.view(F // 32, 2, 32, K)
+        gg = a.float() @ wv[:, 0].reshape(F, K).float().T
+        uu = a.float() @ wv[:, 1].reshape(F, K).float().T
+        sref = torch.nn.functional.silu(gg) * uu
+        assert (s.float() - sref).abs().max().item() < 3e-2 * sref.abs().max().item() + 1e-2
+
+
+@pytest.mark.parametrize("M,N,K", [(512, 6144, 4096), (512, 4096, 4096), (512, 28672, 4096), (512, 4096, 14336),
+                                   (512, 768, 4096), (512, 4096, 512), (512, 3584, 4096), (512, 4096, 1792),
+                                   (512, 16032, 4096), (16384, 6144, 4096), (8, 6144, 4096)])
+def test_gemm_auto_plan(cuda, M, N, K):
+    """The auto plan (possibly split-K) on the Llama-3-8B decode shapes at
+    TP1 and TP8, bit-identical across repeated launches."""
+    g = torch.Generator(device="cuda").manual_seed(M ^ N ^ K)
+    a = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=cuda, generator=g) / K**0.5).to(torch.bfloat16)
+    ws = _ws(cuda)
+    plan, need = ops.gemm_plan(M, N, K, workspace_bytes=ws.numel())
+    assert need <= ws.numel()
+    out = ops.gemm(a, w, workspace=ws)
+    out2 = ops.gemm(a, w, workspace=ws)
+    torch.cuda.synchronize()
+    ref = _ref(a, w)
+    assert (out.float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item() + 1e-2, plan
+    assert torch.equal(out, out2)

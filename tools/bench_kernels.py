@@ -78,8 +78,50 @@ if __name__ == "__main__":
                    + [(M, N, K, TWO | 256) for M, N, K in shapes[3:]])
     if args.what == "gemm":
         bench_gemm([
-            (8192, 6144, 4096, 256), (8192, 4096, 4096, 256), (8192, 28672, 4096, 256),
-            (8192, 4096, 14336, 256), (512, 6144, 4096, 0), (512, 4096, 4096, 0),
+            (16384, 6144, 4096, 0), (16384, 4096, 4096, 0), (16384, 28672, 4096, 0),
+            (16384, 4096, 14336, 0), (512, 6144, 4096, 0), (512, 4096, 4096, 0),
             (512, 28672, 4096, 0), (512, 4096, 14336, 0), (512, 128256, 4096, 0),
             (512, 4096, 4096, 128), (512, 4096, 4096, 64),
         ])
+
+
+def bench_splitk():
+    """Forced (mode, bn, splits) sweep vs the auto plan on decode shapes."""
+    from paper_2503_06433_b200._lib import SSB_GEMM_2SM, SSB_GEMM_SPLIT_SHIFT
+
+    ws = torch.zeros(256 << 20, dtype=torch.uint8, device="cuda")
+    shapes = [(M, N, K) for M in (512, 256) for N, K in
+              ((6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336), (128256, 4096), (768, 4096), (4096, 512),
+               (3584, 4096), (4096, 1792), (16032, 4096))]
+    shapes += [(16384, 6144, 4096), (16384, 4096, 14336), (2048, 4096, 4096)]
+    for M, N, K in shapes:
+        a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        w = (torch.randn(N, K, device="cuda") / K**0.5).to(torch.bfloat16)
+        c = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        fl = 2.0 * M * N * K
+        res = []
+        plan, need = ops.gemm_plan(M, N, K, workspace_bytes=64 << 20)
+        ms = timed(lambda: ops.gemm(a, w, out=c, workspace=ws[: 64 << 20]))
+        res.append(("auto", plan, ms))
+        ms_t = timed(lambda: torch.matmul(a, w.T, out=c))
+        res.append(("cublas", None, ms_t))
+        for mode in (0, 2):
+            for bn in (128, 192, 224, 256):
+                for sp in ((1,) if M > 4096 else (1, 2, 3, 4, 6, 8)):
+                    if K // 64 // sp < 2:
+                        continue
+                    flag = bn | (sp << SSB_GEMM_SPLIT_SHIFT) | (SSB_GEMM_2SM if mode == 2 else 0)
+                    try:
+                        ms = timed(lambda: ops.gemm(a, w, out=c, block_n=flag, workspace=ws), iters=10)
+                    except Exception as e:  # noqa: BLE001
+                        continue
+                    res.append((f"m{mode}b{bn}s{sp}", None, ms))
+        best = min(res[2:], key=lambda r: r[2])
+        print(json.dumps({"M": M, "N": N, "K": K, "auto_plan": res[0][1], "auto_ms": res[0][2],
+                          "auto_tflops": fl / res[0][2] / 1e9, "cublas_ms": ms_t, "cublas_tflops": fl / ms_t / 1e9,
+                          "best": best[0], "best_ms": best[2], "best_tflops": fl / best[2] / 1e9,
+                          "all": {r[0]: round(r[2] * 1e3, 1) for r in res[2:]}}), flush=True)
+
+
+if __name__ == "__main__" and "--what" in sys.argv and sys.argv[sys.argv.index("--what") + 1] == "splitk":
+    bench_splitk()
