@@ -146,16 +146,20 @@ def run_ours(args) -> None:
         return execute(model, hw, reqs, SchedulingPolicy.TRANSITION_MINIMIZING, cfg_p, cfg_d, arch=arch,
                        prompts=prompts, comm=comm, device=dev, worker=worker, max_prefill_tokens=args.prefill_tokens)
 
-    def timed(prompts, k, profile=False):
+    def timed(prompts, k, nvtx=None):
         times, reports = [], []
         for _ in range(k):
             comm.barrier()
             torch.cuda.synchronize(dev)
             s = torch.cuda.Event(enable_timing=True)
             e = torch.cuda.Event(enable_timing=True)
+            if nvtx:  # ncu --nvtx --nvtx-include "<name>/" selects exactly these launches
+                torch.cuda.nvtx.range_push(nvtx)
             s.record()
             rep = one(prompts)
             e.record()
+            if nvtx:
+                torch.cuda.nvtx.range_pop()
             comm.barrier()
             torch.cuda.synchronize(dev)
             times.append(s.elapsed_time(e) / 1e3)
@@ -172,7 +176,7 @@ def run_ours(args) -> None:
     sampler = ClockSampler(local)
     sampler.start()
     launches0 = _lib.STATS.count
-    times, reports = timed(prompts_dev, args.steps)
+    times, reports = timed(prompts_dev, args.steps, nvtx="timed_step")
     launches = (_lib.STATS.count - launches0) // max(args.steps, 1)
     clocks = sampler.stop()
     e2e_times, e2e_reports = timed(prompts_pinned, max(1, min(args.steps, 2)))

@@ -37,6 +37,10 @@ extern "C" {
 #define SSB_EPI_SILU_MUL 2 /* accumulator columns are (32 gate, 32 up) pairs;
                               C[:, j] = silu(gate_j) * up_j, N/2 columns     */
 #define SSB_EPI_F32 3      /* C = A.B^T stored as fp32 (logits)               */
+#define SSB_EPI_ROPE_KV 4  /* QKV projection + RoPE + paged KV append; only
+                              through ssb_gemm_qkv_rope_kv                     */
+#define SSB_EPI_ARGMAX 5   /* per-row (max, argmax) keys; only through
+                              ssb_gemm_lm_head_argmax                         */
 
 const char* ssb_last_error(void);
 int ssb_version(void);
@@ -71,9 +75,11 @@ int ssb_gemm_bf16(const void* A, const void* B, void* C, const void* R, int M, i
  * fp32 partials fit `workspace_bytes`.  Split tiles are reduced inside the
  * kernel by the last-arriving warp of each tile quadrant, summing the
  * partials in split order (deterministic).  The workspace (256-byte aligned
- * device memory) must be ZEROED once before its first use; the kernel leaves
- * its tile counters zero again.  One workspace per stream: concurrent GEMMs
- * must not share it.  This is what lets the skinny decode projections
+ * device memory) starts with a fixed 64 KiB area of tile counters (so at most
+ * 4096 output tiles split) followed by the fp32 partials; it must be ZEROED
+ * once before its first use, and every launch leaves the counter area zero
+ * again, whatever GEMMs of whatever shapes share it.  One workspace per
+ * stream: concurrent GEMMs must not share it.  This is what lets the skinny decode projections
  * (M = batch <= 512 rows, TP-sharded N or K) fill all 148 SMs. */
 int ssb_gemm_bf16_ws(const void* A, const void* B, void* C, const void* R, int M, int N, int K,
                      int lda, int ldb, int ldc, int ldr, int epilogue, int block_n, int max_ctas,
@@ -106,6 +112,20 @@ typedef struct ssb_kv_geometry {
   int block_size; /* tokens per block              */
   int head_dim;   /* elements per head             */
 } ssb_kv_geometry;
+
+/* QKV projection fused with RoPE and the paged KV append (one launch
+ * instead of ssb_gemm_bf16 + ssb_rope_kv_append; same result bit for bit):
+ * qkv[M, (nq+2nk)*head_dim] = A[M,K] . B^T, then q and k heads rotated
+ * (rotate-half, fp32 tables cos/sin[max_pos][head_dim/2]) at positions[m],
+ * and k, v heads of row m written to pool slot slots[m] of local layer
+ * `layer` (slots may be NULL: no append; a negative slot skips the row).
+ * head_dim must be 128.   Replaces the same reference terms as ssb_gemm_bf16
+ * plus the KV write the cost model folds into perf.py:68-86. */
+int ssb_gemm_qkv_rope_kv(const void* A, const void* B, void* qkv, int M, int K, int lda, int ldb, int ldc,
+                         int nq, int nk, int head_dim, const int32_t* positions, const float* rope_cos,
+                         const float* rope_sin, int max_pos, void* pool, ssb_kv_geometry geo,
+                         int layer, const int64_t* slots, int block_n, int max_ctas, void* workspace,
+                         int64_t workspace_bytes, void* stream);
 
 int ssb_kv_reshard_pack(const void* pool, ssb_kv_geometry geo, const int32_t* block_ids, int n_ids,
                         int n_peers, const int32_t* l0, const int32_t* nl, const int32_t* h0,
@@ -215,6 +235,19 @@ int ssb_embedding(const int32_t* ids, int T, const void* table, int vocab_begin,
 int ssb_argmax_rows(const float* logits, int ld, int rows, int cols, int index_base, float* out_val,
                     int32_t* out_idx, void* stream);
 
+/* LM head fused with the greedy argmax: keys[m] = packed (max over the
+ * N columns of A[m].B^T, smallest index of the max + index_base), never
+ * materialising the fp32 logits (M x N x 4 bytes).  keys are zeroed by the
+ * call (stream-ordered) and filled by 64-bit atomicMax from every tile.
+ * Same values and tie rule as ssb_gemm_bf16(SSB_EPI_F32) + ssb_argmax_rows.
+ * Workspace as for ssb_gemm_bf16_ws. */
+int ssb_gemm_lm_head_argmax(const void* A, const void* B, int M, int N, int K, int lda, int ldb,
+                            int index_base, unsigned long long* keys, int block_n, int max_ctas,
+                            void* workspace, int64_t workspace_bytes, void* stream);
+/* keys -> (value, index) arrays for ssb_argmax_combine / the token ids. */
+int ssb_argmax_keys_decode(const unsigned long long* keys, int rows, float* out_val, int32_t* out_idx,
+                           void* stream);
+
 /* Combine n_parts partial argmaxes laid out [n_parts][rows] (vocab-parallel
  * lm_head): largest value, smallest index on ties. */
 int ssb_argmax_combine(const float* vals, const int32_t* idxs, int n_parts, int rows,
@@ -226,8 +259,9 @@ int ssb_argmax_combine(const float* vals, const int32_t* idxs, int n_parts, int 
  * ---------------------------------------------------------------------- */
 /* Causal prefill over packed sequences: qkv[total_tokens, (nq+2nk)*d] (RoPE
  * applied), sequence s spans rows [cu_seqlens[s], cu_seqlens[s+1]);
- * out[T, nq*d].  variant 0 = auto (tcgen05/TMEM kernel for head_dim 128),
- * 1 = the mma.sync kernel (head_dim 64 always uses it). */
+ * out[T, nq*d].  variant 0 = auto (persistent tcgen05/TMEM kernel for
+ * head_dim 128), 1 = the mma.sync kernel (head_dim 64 always uses it),
+ * 2 = the tcgen05 kernel with one CTA per (query tile, head, sequence). */
 int ssb_prefill_attention(const void* qkv, int ld, int total_tokens, int nq, int nk, int head_dim,
                           const int32_t* cu_seqlens, int nseq, int max_len, void* out, int ldo,
                           float softmax_scale, int variant, void* stream);

@@ -16,6 +16,7 @@ SSB_EPI_NONE = 0
 SSB_EPI_RESIDUAL = 1
 SSB_EPI_SILU_MUL = 2
 SSB_EPI_F32 = 3
+SSB_EPI_ROPE_KV = 4
 SSB_GEMM_MC1 = 1 << 16
 SSB_GEMM_MC2 = 1 << 17
 SSB_GEMM_2SM = 1 << 18
@@ -59,6 +60,10 @@ _PI64 = ctypes.POINTER(ctypes.c_int64)
 SIGNATURES: dict[str, list] = {
     "ssb_gemm_bf16": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P],
     "ssb_gemm_bf16_ws": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _I64, _P],
+    "ssb_gemm_qkv_rope_kv": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P, KVGeometry, _I, _P,
+                             _I, _I, _P, _I64, _P],
+    "ssb_gemm_lm_head_argmax": [_P, _P, _I, _I, _I, _I, _I, _I, _P, _I, _I, _P, _I64, _P],
+    "ssb_argmax_keys_decode": [_P, _I, _P, _P, _P],
     "ssb_kv_reshard_pack": [_P, KVGeometry, _P, _I, _I, _PI32, _PI32, _PI32, _PI32, _PI64, _P, _P],
     "ssb_kv_reshard_unpack": [_P, KVGeometry, _P, _I, _I, _PI32, _PI32, _PI32, _PI32, _PI64, _P, _P],
     "ssb_copy2d_batched": [_P, _P, _P, _I, _I64, _P],

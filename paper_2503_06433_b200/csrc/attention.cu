@@ -15,7 +15,7 @@ namespace ssb {
 int encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                         uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
 int launch_prefill_attn_tc(const void* qkv, int ld, int T, int nq, int nk, const int32_t* cu, int nseq,
-                           int max_len, void* out, int ldo, float scale, cudaStream_t s);
+                           int max_len, void* out, int ldo, float scale, cudaStream_t s, bool persistent);
 
 namespace {
 
@@ -484,10 +484,11 @@ int ssb_prefill_attention(const void* qkv, int ld, int total_tokens, int nq, int
   SSB_REQUIRE(ld % 8 == 0 && ldo % 8 == 0 && aligned16(qkv) && aligned16(out), "ssb_prefill_attention: alignment");
   SSB_REQUIRE(total_tokens > 0, "ssb_prefill_attention: total_tokens must be positive");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  // variant 0 = auto (tcgen05 kernel for head_dim 128), 1 = mma.sync kernel
+  // variant 0 = auto (persistent tcgen05 kernel for head_dim 128), 1 = mma.sync kernel,
+  // 2 = tcgen05 kernel with one CTA per (query tile, head, sequence)
   if (head_dim == 128 && variant != 1)
     return launch_prefill_attn_tc(qkv, ld, total_tokens, nq, nk, cu_seqlens, nseq, max_len, out, ldo,
-                                  softmax_scale, s);
+                                  softmax_scale, s, variant != 2);
   switch (head_dim) {
     case 64: return launch_prefill<64>(qkv, ld, nq, nk, cu_seqlens, nseq, max_len, out, ldo, softmax_scale, s);
     case 128: return launch_prefill<128>(qkv, ld, nq, nk, cu_seqlens, nseq, max_len, out, ldo, softmax_scale, s);

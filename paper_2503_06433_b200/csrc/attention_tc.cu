@@ -15,6 +15,8 @@
 //              to smem as bf16 in the UMMA K-major SW128 layout.  The running
 //              max is updated lazily (only when it grows by > 8 in log2
 //              units), so O in TMEM is rescaled rarely; final O / l epilogue.
+#include <algorithm>
+
 #include "common.cuh"
 #include "seesaw_b200.h"
 
@@ -286,14 +288,303 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Persistent variant: one CTA per SM loops over (query tile, head, sequence)
+// work items, longest (most key tiles) first, round-robin across CTAs.  The
+// per-item prologue of the kernel above (TMEM allocation, barrier set-up, the
+// first Q/K/V TMA round trip) and its epilogue are paid once per CTA or
+// hidden: Q is double-buffered in smem so the next item's Q lands while this
+// item computes, and O is double-buffered in TMEM (S0 S1 O0 O1 = 512
+// columns) so the epilogue of item i overlaps the MMAs of item i+1.  All
+// barrier phases run on global counters (key tiles, S tiles, P tiles, items).
+struct SmemP {
+  static constexpr int kQ = 0;                  // 2 buffers
+  static constexpr int kK = 2 * kTile;          // 2 stages
+  static constexpr int kV = kK + 2 * kTile;     // 2 stages
+  static constexpr int kP = kV + 2 * kTile;
+  static constexpr int kBar = kP + kTile;
+  static constexpr int kBytes = kBar + 256 + 1024;
+};
+
+__device__ __forceinline__ bool item_coords(int item, int n_qt_max, int nq, int nseq, const int32_t* cu, int& seq,
+                                            int& h, int& qt, int& start, int& len) {
+  const int per_qt = nq * nseq;
+  qt = n_qt_max - 1 - item / per_qt;  // longest first
+  const int rem = item - (n_qt_max - 1 - qt) * per_qt;
+  seq = rem / nq;
+  h = rem - seq * nq;
+  start = cu[seq];
+  len = cu[seq + 1] - start;
+  return qt * kT < len;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    prefill_attn_tc_persistent(const __grid_constant__ CUtensorMap tmap, const int32_t* __restrict__ cu, int nseq,
+                               int n_qt_max, int nq, int nk, __nv_bfloat16* __restrict__ out, int ldo,
+                               float scale_log2) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemP::kBar);
+  uint64_t* q_full = bars + 0;     // [2]
+  uint64_t* q_empty = bars + 2;    // [2]
+  uint64_t* kv_full = bars + 4;    // [2]
+  uint64_t* kv_empty = bars + 6;   // [2]
+  uint64_t* s_full = bars + 8;     // [2]
+  uint64_t* s_free = bars + 10;    // [2]
+  uint64_t* p_full = bars + 12;
+  uint64_t* o_done = bars + 13;
+  uint64_t* o_free = bars + 14;    // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+
+  const int n_items = n_qt_max * nq * nseq;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int group = nq / nk;
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tmap);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_empty[s], 1);
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_free[s], 4);
+      mbar_init(&o_free[s], 4);
+    }
+    mbar_init(p_full, 4);
+    mbar_init(o_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_s[2] = {tmem, tmem + 128};
+  const uint32_t t_o[2] = {tmem + 256, tmem + 384};
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t keep = policy_evict_last();
+      uint32_t kc = 0, ic = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        int seq, h, qt, start, len;
+        if (!item_coords(item, n_qt_max, nq, nseq, cu, seq, h, qt, start, len)) continue;
+        const int kvh = h / group;
+        const int qcol = h * kD, kcol = (nq + kvh) * kD, vcol = (nq + nk + kvh) * kD;
+        const int qb = ic & 1;
+        mbar_wait(&q_empty[qb], ((ic >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[qb], kTile);
+        for (int s = 0; s < 2; ++s)
+          tma_load_2d(smem + SmemP::kQ + qb * kTile + s * kSub, &tmap, &q_full[qb], qcol + s * 64, start + qt * kT,
+                      keep);
+        for (int j = 0; j <= qt; ++j, ++kc) {
+          const int st = kc & 1;
+          mbar_wait(&kv_empty[st], ((kc >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&kv_full[st], 2 * kTile);
+          for (int s = 0; s < 2; ++s) {
+            tma_load_2d(smem + SmemP::kK + st * kTile + s * kSub, &tmap, &kv_full[st], kcol + s * 64,
+                        start + j * kT, keep);
+            tma_load_2d(smem + SmemP::kV + st * kTile + s * kSub, &tmap, &kv_full[st], vcol + s * 64,
+                        start + j * kT, keep);
+          }
+        }
+        ++ic;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(kT, kT);
+      constexpr uint32_t idesc_o = idesc_bf16_f32(kT, kD) | (1u << 16);  // B (= V) MN-major
+      const uint32_t p_base = smem_u32(smem + SmemP::kP);
+      uint32_t kc = 0, sc = 0, pc = 0, ic = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        int seq, h, qt, start, len;
+        if (!item_coords(item, n_qt_max, nq, nseq, cu, seq, h, qt, start, len)) continue;
+        const int qb = ic & 1;
+        const uint32_t q_base = smem_u32(smem + SmemP::kQ + qb * kTile);
+        const uint32_t o_acc = t_o[qb];
+        mbar_wait(&q_full[qb], (ic >> 1) & 1);
+        // O buffer qb was read out by the epilogue of item ic - 2
+        mbar_wait(&o_free[qb], ((ic >> 1) & 1) ^ 1);
+        int prev_stage = 0;
+        auto pv = [&](int j, int stage) {
+          mbar_wait(p_full, pc & 1);
+          tc_fence_after();
+          const uint32_t v_base = smem_u32(smem + SmemP::kV + stage * kTile);
+#pragma unroll
+          for (int k = 0; k < kT / 16; ++k) {
+            const uint64_t a = sdesc_k_sw128(p_base + (k >> 2) * kSub + (k & 3) * 32);
+            const uint64_t b = sdesc_mn_sw128(v_base + k * 16 * 128, kSub);
+            umma_bf16(o_acc, a, b, idesc_o, (j | k) != 0);
+          }
+          umma_commit(o_done);
+          umma_commit(&kv_empty[stage]);
+          ++pc;
+        };
+        for (int j = 0; j <= qt; ++j, ++kc, ++sc) {
+          const int st = kc & 1;
+          const int ss = sc & 1;
+          mbar_wait(&kv_full[st], (kc >> 1) & 1);
+          mbar_wait(&s_free[ss], ((sc >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t k_base = smem_u32(smem + SmemP::kK + st * kTile);
+#pragma unroll
+          for (int k = 0; k < kD / 16; ++k) {
+            const uint64_t a = sdesc_k_sw128(q_base + (k >> 2) * kSub + (k & 3) * 32);
+            const uint64_t b = sdesc_k_sw128(k_base + (k >> 2) * kSub + (k & 3) * 32);
+            umma_bf16(t_s[ss], a, b, idesc_s, k != 0);
+          }
+          umma_commit(&s_full[ss]);
+          if (j == qt) umma_commit(&q_empty[qb]);  // last read of this Q buffer
+          if (j >= 1) pv(j - 1, prev_stage);
+          prev_stage = st;
+        }
+        pv(qt, prev_stage);
+        ++ic;
+      }
+    }
+  } else {
+    // ---------------- softmax / epilogue: thread = query row ----------------
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    uint8_t* p_row = smem + SmemP::kP + r * 128;
+    uint32_t sc = 0, pc = 0, ic = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      int seq, h, qt, start, len;
+      if (!item_coords(item, n_qt_max, nq, nseq, cu, seq, h, qt, start, len)) continue;
+      const int qb = ic & 1;
+      const uint32_t o_acc = t_o[qb];
+      const int q0 = qt * kT;
+      const int qrow = q0 + r;
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j <= qt; ++j, ++sc) {
+        const int ss = sc & 1;
+        mbar_wait(&s_full[ss], (sc >> 1) & 1);
+        tc_fence_after();
+        float s[kT];
+#pragma unroll
+        for (int c = 0; c < kT / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(t_s[ss] + lane_off + c * 32, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(v[i]) * scale_log2;
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_free[ss]);
+        const int k0 = j * kT;
+        if (j == qt || k0 + kT > len) {
+#pragma unroll
+          for (int i = 0; i < kT; ++i)
+            if (k0 + i > qrow || k0 + i >= len) s[i] = -INFINITY;
+        }
+        float mx = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < kT; ++i) mx = fmaxf(mx, s[i]);
+        float corr = 1.f;
+        const bool rescale = mx > m_used + kRescaleThreshold;
+        if (rescale) {
+          corr = (m_used == -INFINITY) ? 0.f : fast_exp2(m_used - mx);
+          m_used = mx;
+        }
+        float sum = 0.f;
+        uint32_t pk[kT / 2];
+#pragma unroll
+        for (int i = 0; i < kT; i += 2) {
+          const float a = fast_exp2(s[i] - m_used), b = fast_exp2(s[i + 1] - m_used);
+          sum += a + b;
+          pk[i / 2] = pack_bf16x2(a, b);
+        }
+        // the P buffer (and O) are free once the previous P.V completed
+        if (pc > 0) mbar_wait(o_done, (pc - 1) & 1);
+        tc_fence_after();
+        if (j >= 1 && __any_sync(0xffffffffu, rescale)) {
+#pragma unroll 1
+          for (int c = 0; c < kD / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld32(o_acc + lane_off + c * 32, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
+            tmem_st32(o_acc + lane_off + c * 32, v);
+          }
+          tmem_st_wait();
+        }
+        l = l * corr + sum;
+#pragma unroll
+        for (int c = 0; c < kT / 8; ++c) {
+          const int sb = c >> 3, cc = c & 7;
+          uint4 val = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+          *reinterpret_cast<uint4*>(p_row + sb * kSub + ((cc ^ (r & 7)) << 4)) = val;
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full);
+        ++pc;
+      }
+      // epilogue: O / l, then hand the O buffer back to the MMA warp
+      mbar_wait(o_done, (pc - 1) & 1);
+      tc_fence_after();
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      __nv_bfloat16* orow = out + static_cast<size_t>(start + qrow) * ldo + h * kD;
+#pragma unroll 1
+      for (int c = 0; c < kD / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(o_acc + lane_off + c * 32, v);
+        tmem_ld_wait();
+        if (qrow < len) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 o;
+            o.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]) * inv, __uint_as_float(v[8 * q + 1]) * inv);
+            o.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv);
+            o.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv);
+            o.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv);
+            dst[q] = o;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_free[qb]);
+      ++ic;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 }  // namespace
 
 int launch_prefill_attn_tc(const void* qkv, int ld, int T, int nq, int nk, const int32_t* cu, int nseq,
-                           int max_len, void* out, int ldo, float scale, cudaStream_t s) {
+                           int max_len, void* out, int ldo, float scale, cudaStream_t s, bool persistent) {
   CUtensorMap map;
   int rc = encode_tmap_2d_bf16(&map, qkv, static_cast<uint64_t>(ld), static_cast<uint64_t>(T),
                                static_cast<uint64_t>(ld) * 2, 64, kT);
   if (rc) return rc;
+  if (persistent) {
+    static bool pattr = false;
+    if (!pattr) {
+      SSB_CUDA(cudaFuncSetAttribute(prefill_attn_tc_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    SmemP::kBytes));
+      pattr = true;
+    }
+    const int n_qt = (max_len + kT - 1) / kT;
+    const long items = static_cast<long>(n_qt) * nq * nseq;
+    const int grid = static_cast<int>(std::min<long>(num_sms(), items));
+    prefill_attn_tc_persistent<<<grid, kThreads, SmemP::kBytes, s>>>(
+        map, cu, nseq, n_qt, nq, nk, static_cast<__nv_bfloat16*>(out), ldo, scale * 1.4426950408889634f);
+    return check_launch("prefill_attn_tc_persistent");
+  }
   static bool attr = false;
   if (!attr) {
     SSB_CUDA(cudaFuncSetAttribute(prefill_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::kBytes));

@@ -18,6 +18,7 @@
 //               bf16 stores.  Accumulator double buffering lets the epilogue
 //               of tile i overlap the MMAs of tile i+1.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "seesaw_b200.h"
@@ -34,6 +35,7 @@ constexpr int kBK = 64;       // 64 bf16 = 128 B = one swizzle row
 constexpr int kUmmaK = 16;
 constexpr int kThreads = 192;
 constexpr int kGroupM = 16;   // tile rasterisation: 16 M-tiles share a B band in L2
+constexpr size_t kCounterBytes = 64 * 1024;  // split-K tile counters at the head of the workspace
 
 constexpr int pow2_at_least(int x) { return x <= 32 ? 32 : x <= 64 ? 64 : x <= 128 ? 128 : x <= 256 ? 256 : 512; }
 
@@ -51,6 +53,23 @@ struct Cfg {
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
+// SSB_EPI_ROPE_KV: the accumulator columns are the packed [nq | nk | nk]
+// heads (head_dim 128) of a QKV projection.  q and k heads get rotate-half
+// RoPE at positions[row]; k and v heads are also appended to the paged KV
+// pool at slots[row] (negative = skip).  Values are rounded to bf16 BEFORE
+// the rotation, so the result is bit-identical to a bf16 GEMM store followed
+// by ssb_rope_kv_append.
+struct RopeKV {
+  const int32_t* pos;
+  const float* cos;
+  const float* sin;
+  int max_pos;
+  __nv_bfloat16* pool;
+  int n_layers, n_heads, block_size, layer;
+  const int64_t* slots;
+  int nq, nk;
+};
+
 struct Params {
   void* C;
   const void* R;   // residual (may alias C); only for SSB_EPI_RESIDUAL
@@ -59,18 +78,24 @@ struct Params {
   int epi;
   int tiles_m, tiles_n;
   int group_n;     // rasterisation band orientation (see tile_coords)
+  int group_size;  // tiles of the band dimension per band
   // split-K: every output tile is computed as `splits` partial sums over
   // k-block ranges of kb_per_split; the last warp to finish a tile quadrant
   // (counter) reduces the fp32 partials in split order and runs the epilogue
   int splits, kb_per_split;
   float* ws;       // [tiles_m * tiles_n][splits][128][BN] fp32 partials
   int* counters;   // [tiles_m * tiles_n][4], zero between launches (self-resetting)
+  RopeKV rk;       // SSB_EPI_ROPE_KV only
+  int arg_base;    // SSB_EPI_ARGMAX: global index of accumulator column 0
+  int pol_mode;    // L2 cache-policy variant of the operand loads (see producer)
 };
 
 // Grouped rasterisation: kGroupM tiles of the "band" dimension share one
 // operand band in L2 while the other operand streams.  group_n = 0 bands along
 // M (A band resident, B streamed once per band); group_n = 1 bands along N.
-__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int group_n, int& tm, int& tn) {
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int group_n, int group_size, int& tm,
+                                            int& tn) {
+  const int kGroupM = group_size;
   const int band_tiles = group_n ? tiles_n : tiles_m;
   const int other_tiles = group_n ? tiles_m : tiles_n;
   const int per_group = kGroupM * other_tiles;
@@ -157,6 +182,91 @@ __device__ __forceinline__ void store_silu(const Params& p, int row, int col, co
 #pragma unroll
     for (int j = 0; j < 32; ++j)
       if (col + j < ncols) crow[col + j] = __float2bfloat16_rn(silu(g[j]) * u[j]);
+  }
+}
+
+// SSB_EPI_ARGMAX: running (value, index) key of one row over 32 columns.
+// key = orderable(value) << 32 | ~index, so a 64-bit max picks the largest
+// logit and, on ties, the smallest index (ssb_argmax_rows' rule).
+__device__ __forceinline__ unsigned long long argmax_key(float v, int idx) {
+  if (v == 0.f) v = 0.f;  // -0 == +0
+  const uint32_t b = __float_as_uint(v);
+  const uint32_t ord = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+  return (static_cast<unsigned long long>(ord) << 32) | (0xFFFFFFFFu - static_cast<uint32_t>(idx));
+}
+__device__ __forceinline__ void argmax_cols(const Params& p, int col, const float (&f)[32], unsigned long long& best) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    if (col + j < p.N) {
+      const unsigned long long k = argmax_key(f[j], p.arg_base + col + j);
+      best = k > best ? k : best;
+    }
+  }
+}
+
+// RoPE + KV append of one row's 32-column pair (lo = head columns [i0, i0+32),
+// hi = [i0+64, i0+96)) of head `head`, i0 in {0, 32}.
+__device__ __forceinline__ void store_rope(const Params& p, int row, int col_lo, const float (&lo)[32],
+                                           const float (&hi)[32]) {
+  constexpr int kHd = 128, kHalf = 64;
+  const RopeKV& rk = p.rk;
+  const int head = col_lo / kHd;
+  const int i0 = col_lo - head * kHd;
+  __nv_bfloat16* crow = reinterpret_cast<__nv_bfloat16*>(p.C) + static_cast<size_t>(row) * p.ldc;
+  uint32_t olo[16], ohi[16];
+  if (head < rk.nq + rk.nk) {
+    const int ps = min(max(rk.pos[row], 0), rk.max_pos - 1);
+    const float4* cr = reinterpret_cast<const float4*>(rk.cos + static_cast<size_t>(ps) * kHalf + i0);
+    const float4* sr = reinterpret_cast<const float4*>(rk.sin + static_cast<size_t>(ps) * kHalf + i0);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const float4 c4 = __ldg(cr + v), s4 = __ldg(sr + v);
+      const float cc[4] = {c4.x, c4.y, c4.z, c4.w}, ss[4] = {s4.x, s4.y, s4.z, s4.w};
+      float ylo[4], yhi[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float a = __bfloat162float(__float2bfloat16_rn(lo[4 * v + k]));
+        const float b = __bfloat162float(__float2bfloat16_rn(hi[4 * v + k]));
+        ylo[k] = __fsub_rn(__fmul_rn(a, cc[k]), __fmul_rn(b, ss[k]));
+        yhi[k] = __fadd_rn(__fmul_rn(b, cc[k]), __fmul_rn(a, ss[k]));
+      }
+      olo[2 * v] = pack_bf16x2(ylo[0], ylo[1]);
+      olo[2 * v + 1] = pack_bf16x2(ylo[2], ylo[3]);
+      ohi[2 * v] = pack_bf16x2(yhi[0], yhi[1]);
+      ohi[2 * v + 1] = pack_bf16x2(yhi[2], yhi[3]);
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < 16; ++v) {
+      olo[v] = pack_bf16x2(lo[2 * v], lo[2 * v + 1]);
+      ohi[v] = pack_bf16x2(hi[2 * v], hi[2 * v + 1]);
+    }
+  }
+  uint4* dlo = reinterpret_cast<uint4*>(crow + col_lo);
+  uint4* dhi = reinterpret_cast<uint4*>(crow + col_lo + kHalf);
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    dlo[v] = make_uint4(olo[4 * v], olo[4 * v + 1], olo[4 * v + 2], olo[4 * v + 3]);
+    dhi[v] = make_uint4(ohi[4 * v], ohi[4 * v + 1], ohi[4 * v + 2], ohi[4 * v + 3]);
+  }
+  if (head >= rk.nq && rk.slots) {
+    const int64_t slot = rk.slots[row];
+    if (slot >= 0) {
+      const int64_t blk = slot / rk.block_size;
+      const int off = static_cast<int>(slot - blk * rk.block_size);
+      const int kv = head >= rk.nq + rk.nk ? 1 : 0;
+      const int kvh = head - rk.nq - kv * rk.nk;
+      const int64_t plane = static_cast<int64_t>(rk.block_size) * kHd;
+      __nv_bfloat16* dst = rk.pool + ((blk * rk.n_layers + rk.layer) * 2 + kv) * rk.n_heads * plane +
+                           kvh * plane + static_cast<int64_t>(off) * kHd + i0;
+      uint4* plo = reinterpret_cast<uint4*>(dst);
+      uint4* phi = reinterpret_cast<uint4*>(dst + kHalf);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        plo[v] = make_uint4(olo[4 * v], olo[4 * v + 1], olo[4 * v + 2], olo[4 * v + 3]);
+        phi[v] = make_uint4(ohi[4 * v], ohi[4 * v + 1], ohi[4 * v + 2], ohi[4 * v + 3]);
+      }
+    }
   }
 }
 
@@ -258,13 +368,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------- TMA producer ----------------
       // the banded operand is re-read by every tile of its band: keep it in
       // L2; the streamed operand is read by the band's tiles in one wave
-      const uint64_t pol_a = p.group_n ? policy_evict_first() : policy_evict_last();
-      const uint64_t pol_b = p.group_n ? policy_evict_last() : policy_evict_first();
+      // L2 policy of the operand loads (SSB_GEMM_POLICY): 2 (default) = both
+      // evict_last; 0 = banded operand evict_last + streamed operand
+      // evict_first; 1 = both evict_normal; 3 = streamed operand evict_normal.
+      // Measured on the 8B prefill projections (tools/gemm_traffic.sh,
+      // tools/gemm_sustained.py): evict_first on the streamed operand lets its
+      // tiles leave L2 before the band's other tiles reuse them (gate/up: 8-9
+      // GB of DRAM reads per launch vs 3.3-3.9 GB with 2), and under the 1 kW
+      // cap that DRAM power costs SM clock: mode 2 is +5% sustained TFLOP/s.
+      uint64_t pol_a, pol_b;
+      if (p.pol_mode == 1) {
+        pol_a = pol_b = policy_evict_normal();
+      } else if (p.pol_mode == 2) {
+        pol_a = pol_b = policy_evict_last();
+      } else {
+        const uint64_t stream_pol = p.pol_mode == 3 ? policy_evict_normal() : policy_evict_first();
+        pol_a = p.group_n ? stream_pol : policy_evict_last();
+        pol_b = p.group_n ? policy_evict_last() : stream_pol;
+      }
       int stage = 0;
       uint32_t phase = 0;
       for (int u = cid; u < num_units; u += nclusters) {
         int um, tn;
-        tile_coords(u / p.splits, units_m, p.tiles_n, p.group_n, um, tn);
+        tile_coords(u / p.splits, units_m, p.tiles_n, p.group_n, p.group_size, um, tn);
         const int tm = um * MC + crank;
         const int kb0 = (u % p.splits) * p.kb_per_split;
         const int kb1 = min(num_kb, kb0 + p.kb_per_split);
@@ -357,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int u = cid; u < num_units; u += nclusters) {
       int um, tn;
       const int t = u / p.splits;
-      tile_coords(t, units_m, p.tiles_n, p.group_n, um, tn);
+      tile_coords(t, units_m, p.tiles_n, p.group_n, p.group_size, um, tn);
       const int tm = um * MC + crank;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -365,7 +491,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool row_ok = row < p.M;
       const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       if (p.splits == 1) {
-        if (p.epi == SSB_EPI_SILU_MUL) {
+        if (p.epi == SSB_EPI_ARGMAX) {
+          unsigned long long best = 0;
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t a[32];
+            tmem_ld32(tbase + c * 32, a);
+            tmem_ld_wait();
+            float f[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(a[j]);
+            argmax_cols(p, tn * BN + c * 32, f, best);
+          }
+          if (row_ok && best) atomicMax(reinterpret_cast<unsigned long long*>(p.C) + row, best);
+        } else if (p.epi == SSB_EPI_ROPE_KV) {
+          // per 128-column head: chunk pairs (0, 2) and (1, 3) are the
+          // rotate-half partners (i, i + 64)
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            if (c & 2) continue;
+            uint32_t lo[32], hi[32];
+            tmem_ld32(tbase + c * 32, lo);
+            tmem_ld32(tbase + (c + 2) * 32, hi);
+            tmem_ld_wait();
+            float fl[32], fh[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              fl[j] = __uint_as_float(lo[j]);
+              fh[j] = __uint_as_float(hi[j]);
+            }
+            if (row_ok && tn * BN + c * 32 < p.N) store_rope(p, row, tn * BN + c * 32, fl, fh);
+          }
+        } else if (p.epi == SSB_EPI_SILU_MUL) {
           // accumulator columns come in (32 gate, 32 up) pairs -> 32 outputs
 #pragma unroll 1
           for (int c = 0; c < BN / 64; ++c) {
@@ -438,7 +595,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) p.counters[tile * 4 + q] = 0;  // every split arrived: reset for the next launch
           const float4* rbase = reinterpret_cast<const float4*>(p.ws) +
                                 static_cast<size_t>(tile) * p.splits * split_stride4 + q * 32 + lane;
-          if (p.epi == SSB_EPI_SILU_MUL) {
+          if (p.epi == SSB_EPI_ARGMAX) {
+            unsigned long long best = 0;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+              float f[32];
+              sum_partials(rbase, split_stride4, p.splits, c * 8, f);
+              argmax_cols(p, tn * BN + c * 32, f, best);
+            }
+            if (row_ok && best) atomicMax(reinterpret_cast<unsigned long long*>(p.C) + row, best);
+          } else if (p.epi == SSB_EPI_ROPE_KV) {
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+              if (c & 2) continue;
+              float fl[32], fh[32];
+              sum_partials(rbase, split_stride4, p.splits, c * 8, fl);
+              sum_partials(rbase, split_stride4, p.splits, (c + 2) * 8, fh);
+              if (row_ok && tn * BN + c * 32 < p.N) store_rope(p, row, tn * BN + c * 32, fl, fh);
+            }
+          } else if (p.epi == SSB_EPI_SILU_MUL) {
 #pragma unroll 1
             for (int c = 0; c < BN / 64; ++c) {
               float g[32], v[32];
@@ -474,9 +649,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Experiment knobs read once from the environment (tools/gemm_sustained.py).
+int gemm_env(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+int gemm_policy_mode() {
+  static const int mode = gemm_env("SSB_GEMM_POLICY", 2);
+  return mode;
+}
+
 template <int BN, int MODE>
 int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, int K, int lda,
-           int ldb, int ldc, int ldr, int epi, cudaStream_t stream, int max_ctas, int splits, void* ws) {
+           int ldb, int ldc, int ldr, int epi, cudaStream_t stream, int max_ctas, int splits, void* ws,
+           const RopeKV* rk, int arg_base) {
   using C = Cfg<BN, MODE>;
   constexpr int MC = MODE ? 2 : 1;
   CUtensorMap ta, tb;
@@ -499,26 +685,30 @@ int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, 
   p.ldc = ldc;
   p.ldr = ldr;
   p.epi = epi;
+  if (rk) p.rk = *rk;
+  p.arg_base = arg_base;
+  p.pol_mode = gemm_policy_mode();
   p.tiles_m = (M + kBM - 1) / kBM;
   p.tiles_n = (N + BN - 1) / BN;
   const int num_kb = (K + kBK - 1) / kBK;
   p.kb_per_split = (num_kb + splits - 1) / splits;
   p.splits = (num_kb + p.kb_per_split - 1) / p.kb_per_split;  // no empty split
+  // workspace = a FIXED counter area (kCounterBytes, shared by every GEMM
+  // that uses this workspace, so its zero invariant survives GEMMs of
+  // different tile counts) followed by this launch's fp32 partials
   p.counters = static_cast<int*>(ws);
-  p.ws = nullptr;
-  if (p.splits > 1) {
-    // a pair's second CTA may own a phantom M tile past the end (tiles_m odd)
-    const size_t tiles_alloc = static_cast<size_t>((p.tiles_m + MC - 1) / MC * MC) * p.tiles_n;
-    const size_t cnt_bytes = (tiles_alloc * 4 * sizeof(int) + 255) & ~size_t(255);
-    p.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + cnt_bytes);
-  }
+  p.ws = p.splits > 1 ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kCounterBytes) : nullptr;
   // band the operand whose re-streaming would cost more DRAM traffic:
   // M-bands re-read B once per band, N-bands re-read A once per band
   {
     const double a_bytes = 2.0 * M * K, b_bytes = 2.0 * N * K;
-    const double m_band = a_bytes + b_bytes * ((p.tiles_m + kGroupM - 1) / kGroupM);
-    const double n_band = b_bytes + a_bytes * ((p.tiles_n + kGroupM - 1) / kGroupM);
+    static const int group_env = gemm_env("SSB_GEMM_GROUP", kGroupM);
+    static const int band_env = gemm_env("SSB_GEMM_BAND", -1);
+    p.group_size = group_env;
+    const double m_band = a_bytes + b_bytes * ((p.tiles_m + p.group_size - 1) / p.group_size);
+    const double n_band = b_bytes + a_bytes * ((p.tiles_n + p.group_size - 1) / p.group_size);
     p.group_n = n_band < m_band ? 1 : 0;
+    if (band_env >= 0) p.group_n = band_env;
   }
   const long units = static_cast<long>((p.tiles_m + MC - 1) / MC) * p.tiles_n * p.splits;
   int grid = num_sms();
@@ -548,11 +738,19 @@ struct Plan {
   int mode, bn, splits;
 };
 
+// Tiles (128-row, including a pair's phantom tile when tiles_m is odd).
+size_t plan_tiles(int M, int N, const Plan& pl) {
+  const int MC = pl.mode ? 2 : 1;
+  return static_cast<size_t>(((M + kBM * MC - 1) / (kBM * MC)) * MC) * ((N + pl.bn - 1) / pl.bn);
+}
+
+// Workspace bytes of a split plan; SIZE_MAX when the tile counters do not fit
+// the fixed counter area.
 size_t plan_ws_bytes(int M, int N, const Plan& pl) {
   if (pl.splits <= 1) return 0;
-  const int MC = pl.mode ? 2 : 1;
-  const size_t tiles = static_cast<size_t>(((M + kBM * MC - 1) / (kBM * MC)) * MC) * ((N + pl.bn - 1) / pl.bn);
-  return ((tiles * 4 * sizeof(int) + 255) & ~size_t(255)) + tiles * pl.splits * kBM * pl.bn * sizeof(float);
+  const size_t tiles = plan_tiles(M, N, pl);
+  if (tiles * 4 * sizeof(int) > kCounterBytes) return SIZE_MAX;
+  return kCounterBytes + tiles * pl.splits * kBM * pl.bn * sizeof(float);
 }
 
 // Modelled time (microseconds) of one configuration: a fixed launch /
@@ -591,12 +789,14 @@ Plan choose_plan(int M, int N, int K, int epi, int sms, size_t ws_bytes) {
   double best_t = 1e30;
   const int bns[4] = {256, 224, 192, 128};
   const int kb = (K + kBK - 1) / kBK;
+  static const int no_split = gemm_env("SSB_GEMM_NO_SPLIT", 0);
   for (int mode = 0; mode <= 2; mode += 2) {
     if (mode == 2 && M <= kBM) continue;
     for (int bn : bns) {
       if (epi == SSB_EPI_SILU_MUL && bn % 64) continue;  // gate/up pairs of 32 columns
+      if (epi == SSB_EPI_ROPE_KV && bn % 128) continue;  // whole heads per tile
       for (int sp = 1; sp <= 16; ++sp) {
-        if (sp > 1 && (kb / sp < 4)) break;
+        if (sp > 1 && (kb / sp < 4 || no_split)) break;
         Plan pl{mode, bn, sp};
         if (sp > 1 && plan_ws_bytes(M, N, pl) > ws_bytes) break;
         const double t = plan_cost(M, N, K, sms, pl);
@@ -616,19 +816,22 @@ Plan choose_plan(int M, int N, int K, int epi, int sms, size_t ws_bytes) {
 namespace {
 int gemm_entry(const void* A, const void* B, void* C, const void* R, int M, int N, int K, int lda, int ldb,
                int ldc, int ldr, int epilogue, int block_n, int max_ctas, void* workspace, int64_t ws_bytes,
-               void* stream) {
+               void* stream, const ssb::RopeKV* rk = nullptr, int arg_base = 0) {
   using namespace ssb;
   SSB_REQUIRE(M > 0 && N > 0 && K > 0, "ssb_gemm_bf16: empty problem M=%d N=%d K=%d", M, N, K);
   SSB_REQUIRE(A && B && C, "ssb_gemm_bf16: null operand");
-  SSB_REQUIRE(epilogue >= SSB_EPI_NONE && epilogue <= SSB_EPI_F32, "ssb_gemm_bf16: bad epilogue %d",
-              epilogue);
+  SSB_REQUIRE((epilogue >= SSB_EPI_NONE && epilogue <= SSB_EPI_F32) || (epilogue == SSB_EPI_ROPE_KV && rk) ||
+                  epilogue == SSB_EPI_ARGMAX,
+              "ssb_gemm_bf16: bad epilogue %d", epilogue);
   SSB_REQUIRE(epilogue != SSB_EPI_RESIDUAL || R, "ssb_gemm_bf16: residual epilogue without R");
   SSB_REQUIRE(lda >= K && ldb >= K, "ssb_gemm_bf16: lda/ldb smaller than K");
-  SSB_REQUIRE(epilogue == SSB_EPI_SILU_MUL ? (N % 64 == 0 && ldc >= N / 2) : ldc >= N,
+  SSB_REQUIRE(epilogue == SSB_EPI_SILU_MUL ? (N % 64 == 0 && ldc >= N / 2)
+                                          : (epilogue == SSB_EPI_ARGMAX || ldc >= N),
               "ssb_gemm_bf16: bad ldc/N for epilogue");
   SSB_REQUIRE(ws_bytes >= 0 && (ws_bytes == 0 || workspace), "ssb_gemm_bf16: bad workspace");
   if (!aligned16(A) || !aligned16(B) || (lda % 8) || (ldb % 8) || !aligned16(C) ||
-      (ldc % (epilogue == SSB_EPI_F32 ? 4 : 8)) || (R && (!aligned16(R) || (ldr % 8))) ||
+      (epilogue != SSB_EPI_ARGMAX && (ldc % (epilogue == SSB_EPI_F32 ? 4 : 8))) ||
+      (R && (!aligned16(R) || (ldr % 8))) ||
       (workspace && (reinterpret_cast<uintptr_t>(workspace) & 255))) {
     set_error("ssb_gemm_bf16: operands must be 16-byte aligned with leading dims %% 8 == 0 "
               "(workspace 256-byte aligned)");
@@ -648,6 +851,8 @@ int gemm_entry(const void* A, const void* B, void* C, const void* R, int M, int 
   }
   if (epilogue == SSB_EPI_SILU_MUL && pl.bn % 64)
     return fail_arg("ssb_gemm_bf16: SiLU epilogue needs block_n %% 64 == 0");
+  if (epilogue == SSB_EPI_ROPE_KV && pl.bn % 128)
+    return fail_arg("ssb_gemm_qkv_rope_kv: block_n must be 128 or 256 (whole heads per tile)");
   if (pl.splits > 1) {  // effective split count: no empty k-range
     const int kb = (K + kBK - 1) / kBK, kbs = (kb + pl.splits - 1) / pl.splits;
     pl.splits = (kb + kbs - 1) / kbs;
@@ -658,11 +863,11 @@ int gemm_entry(const void* A, const void* B, void* C, const void* R, int M, int 
 #define SSB_GEMM_CASE(BN_)                                                                              \
   case BN_:                                                                                            \
     return pl.mode == 2   ? launch<BN_, 2>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas, \
-                                           pl.splits, workspace)                                       \
+                                           pl.splits, workspace, rk, arg_base)                         \
            : pl.mode == 1 ? launch<BN_, 1>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas, \
-                                           pl.splits, workspace)                                       \
+                                           pl.splits, workspace, rk, arg_base)                         \
                           : launch<BN_, 0>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas, \
-                                           pl.splits, workspace);
+                                           pl.splits, workspace, rk, arg_base);
   switch (pl.bn) {
     SSB_GEMM_CASE(256)
     SSB_GEMM_CASE(224)
@@ -699,4 +904,47 @@ extern "C" int64_t ssb_gemm_plan(int M, int N, int K, int epilogue, int max_ctas
     out_plan[2] = pl.splits;
   }
   return static_cast<int64_t>(plan_ws_bytes(M, N, pl));
+}
+
+extern "C" int ssb_gemm_qkv_rope_kv(const void* A, const void* B, void* qkv, int M, int K, int lda, int ldb,
+                                    int ldc, int nq, int nk, int head_dim, const int32_t* positions,
+                                    const float* rope_cos, const float* rope_sin, int max_pos, void* pool,
+                                    ssb_kv_geometry geo, int layer, const int64_t* slots, int block_n,
+                                    int max_ctas, void* workspace, int64_t workspace_bytes, void* stream) {
+  using namespace ssb;
+  SSB_REQUIRE(head_dim == 128, "ssb_gemm_qkv_rope_kv: head_dim must be 128 (got %d)", head_dim);
+  SSB_REQUIRE(nq > 0 && nk > 0 && nq % nk == 0, "ssb_gemm_qkv_rope_kv: bad head counts nq=%d nk=%d", nq, nk);
+  SSB_REQUIRE(positions && rope_cos && rope_sin && max_pos > 0, "ssb_gemm_qkv_rope_kv: null RoPE table");
+  SSB_REQUIRE(!slots || (pool && geo.n_heads == nk && geo.head_dim == head_dim && layer >= 0 &&
+                         layer < geo.n_layers && geo.block_size > 0),
+              "ssb_gemm_qkv_rope_kv: pool geometry does not match (nk=%d, heads=%d, layer=%d of %d)", nk,
+              geo.n_heads, layer, geo.n_layers);
+  SSB_REQUIRE(!pool || aligned16(pool), "ssb_gemm_qkv_rope_kv: pool must be 16-byte aligned");
+  RopeKV rk;
+  rk.pos = positions;
+  rk.cos = rope_cos;
+  rk.sin = rope_sin;
+  rk.max_pos = max_pos;
+  rk.pool = static_cast<__nv_bfloat16*>(pool);
+  rk.n_layers = geo.n_layers;
+  rk.n_heads = geo.n_heads;
+  rk.block_size = geo.block_size;
+  rk.layer = layer;
+  rk.slots = slots;
+  rk.nq = nq;
+  rk.nk = nk;
+  const int N = (nq + 2 * nk) * head_dim;
+  return gemm_entry(A, B, qkv, nullptr, M, N, K, lda, ldb, ldc, 0, SSB_EPI_ROPE_KV, block_n, max_ctas, workspace,
+                    workspace_bytes, stream, &rk);
+}
+
+extern "C" int ssb_gemm_lm_head_argmax(const void* A, const void* B, int M, int N, int K, int lda, int ldb,
+                                       int index_base, unsigned long long* keys, int block_n, int max_ctas,
+                                       void* workspace, int64_t workspace_bytes, void* stream) {
+  using namespace ssb;
+  SSB_REQUIRE(keys, "ssb_gemm_lm_head_argmax: null keys");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  SSB_CUDA(cudaMemsetAsync(keys, 0, static_cast<size_t>(M) * sizeof(unsigned long long), s));
+  return gemm_entry(A, B, keys, nullptr, M, N, K, lda, ldb, 0, 0, SSB_EPI_ARGMAX, block_n, max_ctas, workspace,
+                    workspace_bytes, stream, nullptr, index_base);
 }

@@ -186,6 +186,17 @@ __global__ void argmax_combine_kernel(const float* __restrict__ vals, const int3
   out[row] = bi;
 }
 
+__global__ void argmax_keys_kernel(const unsigned long long* __restrict__ keys, int rows, float* __restrict__ ov,
+                                   int32_t* __restrict__ oi) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  const unsigned long long k = keys[row];
+  const uint32_t ord = static_cast<uint32_t>(k >> 32);
+  const uint32_t b = (ord & 0x80000000u) ? (ord & 0x7FFFFFFFu) : ~ord;
+  ov[row] = __uint_as_float(b);
+  oi[row] = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(k & 0xFFFFFFFFu));
+}
+
 __global__ void decode_positions_kernel(int32_t* __restrict__ ctx, const int32_t* __restrict__ tables,
                                         int max_blocks, int block_size, int32_t* __restrict__ pos,
                                         int64_t* __restrict__ slots, int B) {
@@ -279,3 +290,13 @@ int ssb_argmax_combine(const float* vals, const int32_t* idxs, int n_parts, int 
 }
 
 }  // extern "C"
+
+int ssb_argmax_keys_decode(const unsigned long long* keys, int rows, float* out_val, int32_t* out_idx,
+                           void* stream) {
+  using namespace ssb;
+  SSB_REQUIRE(rows >= 0 && keys && out_val && out_idx, "ssb_argmax_keys_decode: bad arguments");
+  if (rows == 0) return 0;
+  argmax_keys_kernel<<<(rows + 127) / 128, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(keys, rows, out_val,
+                                                                                            out_idx);
+  return check_launch("ssb_argmax_keys_decode");
+}

@@ -21,6 +21,7 @@ struct PeerTable {
   int32_t l0[SSB_MAX_PEERS], nl[SSB_MAX_PEERS], h0[SSB_MAX_PEERS], nh[SSB_MAX_PEERS];
   int64_t off[SSB_MAX_PEERS];
   int32_t run_begin[SSB_MAX_PEERS + 1];  // prefix of n_ids*nl*2 runs per peer
+  int32_t uniform_nl;                    // > 0: every peer has this nl and nh > 0
 };
 
 constexpr int kCopyThreads = 256;
@@ -59,13 +60,26 @@ __global__ void __launch_bounds__(kCopyThreads) kv_reshard_kernel(
     uint8_t* __restrict__ pool, uint8_t* __restrict__ staging, const int32_t* __restrict__ ids,
     int n_ids, int n_peers, ssb_kv_geometry geo, const PeerTable tab) {
   const int run = blockIdx.x;
-  int p = 0;
-  while (p + 1 < n_peers && run >= tab.run_begin[p + 1]) ++p;
-  const int local = run - tab.run_begin[p];
-  const int nl = tab.nl[p];
-  const int kv = local & 1;
-  const int j = (local >> 1) % nl;
-  const int i = (local >> 1) / nl;
+  int p = 0, kv, j, i, nl;
+  if (kPack && tab.uniform_nl > 0) {
+    // every peer takes the same layer range length: walk the pool in address
+    // order (block, layer, K|V, then peers = adjacent head planes) so
+    // consecutive CTAs read consecutive planes; the staging writes scatter
+    // over the peers' regions in 16 KiB+ runs instead
+    nl = tab.uniform_nl;
+    p = run % n_peers;
+    const int rest = run / n_peers;
+    kv = rest & 1;
+    j = (rest >> 1) % nl;
+    i = (rest >> 1) / nl;
+  } else {
+    while (p + 1 < n_peers && run >= tab.run_begin[p + 1]) ++p;
+    const int local = run - tab.run_begin[p];
+    nl = tab.nl[p];
+    kv = local & 1;
+    j = (local >> 1) % nl;
+    i = (local >> 1) / nl;
+  }
   const int64_t plane = static_cast<int64_t>(geo.block_size) * geo.head_dim * 2;  // bytes / head
   const int64_t run_bytes = plane * tab.nh[p];
   const int64_t blk = ids[i];
@@ -113,6 +127,9 @@ int kv_reshard(bool pack, void* pool, ssb_kv_geometry geo, const int32_t* ids, i
     runs += n_ids * t.nl[p] * 2;
   }
   t.run_begin[n_peers] = runs;
+  t.uniform_nl = t.nl[0];
+  for (int p = 1; p < n_peers; ++p)
+    if (t.nl[p] != t.nl[0]) t.uniform_nl = 0;
   if (runs == 0) return 0;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (pack)

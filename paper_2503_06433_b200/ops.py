@@ -25,6 +25,9 @@ def gemm_plan(M: int, N: int, K: int, epilogue: int = SSB_EPI_NONE, max_ctas: in
     return (out[0], out[1], out[2]), int(need)
 
 
+_PREFILL_VARIANT = int(__import__("os").environ.get("SSB_PREFILL_ATTN_VARIANT", "0"))
+
+
 def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
@@ -216,6 +219,50 @@ def rope_kv_append(qkv: torch.Tensor, nq: int, nk: int, positions: torch.Tensor,
          slots.data_ptr() if slots is not None else None, _stream())
 
 
+def gemm_qkv_rope_kv(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor, nq: int, nk: int,
+                     positions: torch.Tensor, rope_cos: torch.Tensor, rope_sin: torch.Tensor,
+                     pool: torch.Tensor | None, geometry, layer: int, slots: torch.Tensor | None,
+                     block_n: int = 0, max_ctas: int = 0, workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """QKV projection with RoPE and the paged K/V append fused into the GEMM
+    epilogue: bit-identical to gemm() followed by rope_kv_append()."""
+    _check(a, "a")
+    _check(w, "w")
+    _check(out, "out")
+    M, K = a.shape
+    d = rope_cos.shape[1] * 2
+    if w.shape[0] != (nq + 2 * nk) * d or w.shape[1] != K:
+        raise ValueError(f"gemm_qkv_rope_kv: weight {tuple(w.shape)} is not [(nq+2nk)*{d}, {K}]")
+    if positions.dtype != torch.int32 or rope_cos.dtype != torch.float32:
+        raise ValueError("gemm_qkv_rope_kv: positions int32, tables float32")
+    if slots is not None and slots.dtype != torch.int64:
+        raise ValueError("gemm_qkv_rope_kv: slots must be int64")
+    call("ssb_gemm_qkv_rope_kv", a.data_ptr(), w.data_ptr(), out.data_ptr(), M, K, a.stride(0), w.stride(0),
+         out.stride(0), nq, nk, d, positions.data_ptr(), rope_cos.data_ptr(), rope_sin.data_ptr(),
+         rope_cos.shape[0], pool.data_ptr() if pool is not None else None, _lib.KVGeometry(*geometry), layer,
+         slots.data_ptr() if slots is not None else None, block_n, max_ctas,
+         workspace.data_ptr() if workspace is not None else None,
+         workspace.numel() * workspace.element_size() if workspace is not None else 0, _stream())
+    return out
+
+
+def lm_head_argmax(h: torch.Tensor, w: torch.Tensor, index_base: int, out_val: torch.Tensor,
+                   out_idx: torch.Tensor, keys: torch.Tensor | None = None,
+                   workspace: torch.Tensor | None = None) -> None:
+    """Greedy argmax of h @ w.T without materialising the logits: the GEMM
+    epilogue reduces each row to a packed (value, index) key (64-bit
+    atomicMax), then the keys are unpacked to (value, index + index_base)."""
+    _check(h, "h")
+    _check(w, "w")
+    M, K = h.shape
+    N = w.shape[0]
+    if keys is None:
+        keys = torch.empty(M, dtype=torch.int64, device=h.device)
+    call("ssb_gemm_lm_head_argmax", h.data_ptr(), w.data_ptr(), M, N, K, h.stride(0), w.stride(0), index_base,
+         keys.data_ptr(), 0, 0, workspace.data_ptr() if workspace is not None else None,
+         workspace.numel() * workspace.element_size() if workspace is not None else 0, _stream())
+    call("ssb_argmax_keys_decode", keys.data_ptr(), M, out_val.data_ptr(), out_idx.data_ptr(), _stream())
+
+
 def embedding(ids: torch.Tensor, table: torch.Tensor, vocab_begin: int, out: torch.Tensor) -> torch.Tensor:
     _check(table, "table")
     if ids.dtype != torch.int32:
@@ -238,9 +285,11 @@ def argmax_combine(vals: torch.Tensor, idxs: torch.Tensor, out_idx: torch.Tensor
 
 
 def prefill_attention(qkv: torch.Tensor, nq: int, nk: int, head_dim: int, cu_seqlens: torch.Tensor,
-                      max_len: int, out: torch.Tensor, scale: float, variant: int = 0) -> torch.Tensor:
+                      max_len: int, out: torch.Tensor, scale: float, variant: int | None = None) -> torch.Tensor:
     """Causal varlen attention over packed prompts (variant 0: tcgen05 kernel
     for head_dim 128; 1: mma.sync kernel)."""
+    if variant is None:  # SSB_PREFILL_ATTN_VARIANT: A/B switch of the kernel variant
+        variant = _PREFILL_VARIANT
     _check(qkv, "qkv")
     _check(out, "out")
     if cu_seqlens.dtype != torch.int32:

@@ -123,6 +123,10 @@ class Worker:
         self.decode_lanes = int(os.environ.get("SSB_DECODE_LANES", "1"))
         self.lane_gemm_cap = int(os.environ.get("SSB_LANE_GEMM_CAP", "0"))
         self.min_lane_rows = int(os.environ.get("SSB_MIN_LANE_ROWS", "64"))
+        # RoPE + K/V append in the QKV GEMM epilogue (head_dim 128)
+        self.fuse_rope = os.environ.get("SSB_FUSE_ROPE", "1") != "0"
+        # greedy argmax in the LM-head GEMM epilogue
+        self.fuse_argmax = os.environ.get("SSB_FUSE_ARGMAX", "1") != "0"
 
     # ------------------------------------------------------------ layouts --
     def _tp_comm(self, cfg: ParallelismConfig, stage: int) -> Comm:
@@ -295,17 +299,28 @@ class Worker:
         wl = self.state.weights
         return range(wl.layer_begin, wl.layer_end)
 
-    def _block(self, x: torch.Tensor, layer: int, attn_fn, buf: dict, cap: int = 0) -> None:
+    def _block(self, x: torch.Tensor, layer: int, attn_fn, buf: dict, rope: tuple, cap: int = 0) -> None:
         """One transformer layer on x (in place); attn_fn(qkv, layer_local) -> attn out.
-        ``cap`` bounds the GEMMs' persistent grid (decode lane overlap)."""
+        ``rope`` = (positions, slots) of the rows: RoPE and the paged K/V
+        append run in the QKV GEMM's epilogue (head_dim 128) or as a separate
+        kernel.  ``cap`` bounds the GEMMs' persistent grid (decode lane overlap)."""
         st = self.state
         eps = self.arch.rms_eps
         p = f"L{layer}."
         lead = st.rank == 0
         ws = buf["ws"]
+        local = layer - st.weights.layer_begin
+        nq, nk = st.weights.n_q_heads, st.weights.n_kv_heads
+        pos, slots = rope
+        geo = self.geometry().as_tuple()
         h = ops.rmsnorm(x, self.w(p + "attn_norm"), eps, out=buf["h"])
-        qkv = ops.gemm(h, self.w(p + "wqkv"), out=buf["qkv"], max_ctas=cap, workspace=ws)
-        attn = attn_fn(qkv, layer - st.weights.layer_begin)
+        if self.fuse_rope and self.arch.head_dim == 128:
+            qkv = ops.gemm_qkv_rope_kv(h, self.w(p + "wqkv"), buf["qkv"], nq, nk, pos, self.rope_cos, self.rope_sin,
+                                       self.pool, geo, local, slots, max_ctas=cap, workspace=ws)
+        else:
+            qkv = ops.gemm(h, self.w(p + "wqkv"), out=buf["qkv"], max_ctas=cap, workspace=ws)
+            ops.rope_kv_append(qkv, nq, nk, pos, self.rope_cos, self.rope_sin, self.pool, geo, local, slots)
+        attn = attn_fn(qkv, local)
         ops.gemm(attn, self.w(p + "wo"), out=x, residual=x if lead else None, max_ctas=cap, workspace=ws)
         self._reduce_into(x)
         h = ops.rmsnorm(x, self.w(p + "mlp_norm"), eps, out=buf["h"])
@@ -346,12 +361,16 @@ class Worker:
         """Vocab-parallel LM head + greedy argmax (fp32 logits)."""
         st = self.state
         n = h_last.shape[0]
-        logits = ops.gemm(h_last, self.w("head"), out_f32=True, workspace=ws)
         vals = torch.empty(n, dtype=torch.float32, device=self.device)
         idxs = torch.empty(n, dtype=torch.int32, device=self.device)
-        ops.argmax_rows(logits, st.weights.vocab_begin, vals, idxs)
-        if self.record_logits:
-            self._record(logits)
+        if self.record_logits or not self.fuse_argmax:
+            logits = ops.gemm(h_last, self.w("head"), out_f32=True, workspace=ws)
+            ops.argmax_rows(logits, st.weights.vocab_begin, vals, idxs)
+            if self.record_logits:
+                self._record(logits)
+        else:
+            # argmax in the LM-head GEMM epilogue: no [n, vocab] fp32 logits round trip
+            ops.lm_head_argmax(h_last, self.w("head"), st.weights.vocab_begin, vals, idxs, workspace=ws)
         if st.tp_comm.size == 1:
             out_tokens.copy_(idxs)
             return
@@ -403,12 +422,10 @@ class Worker:
         nq, nk = st.weights.n_q_heads, st.weights.n_kv_heads
 
         def attn(qkv, layer_local):
-            ops.rope_kv_append(qkv, nq, nk, pos_d, self.rope_cos, self.rope_sin, self.pool, geo.as_tuple(),
-                               layer_local, slots_d)
             return ops.prefill_attention(qkv, nq, nk, a.head_dim, cu_d, max_len, buf["attn"], self.scale)
 
         for layer in self._layers():
-            self._block(x, layer, attn, buf)
+            self._block(x, layer, attn, buf, (pos_d, slots_d))
         if st.stage < st.cfg.pp - 1:
             self.replica_comm.send(x, st.pp_next)
             return
@@ -461,16 +478,14 @@ class Worker:
                     st.tp_comm.all_reduce_(x)
 
                 def attn(qkv, layer_local, v=v, buf=buf):
-                    ops.rope_kv_append(qkv, nq, nk, v["pos"], self.rope_cos, self.rope_sin, self.pool,
-                                       geo.as_tuple(), layer_local, v["slot"])
                     return ops.decode_attention(qkv, nq, nk, self.pool, geo.as_tuple(), self.num_blocks,
                                                 layer_local, v["tab"], v["ctx"], buf["attn"], self.scale)
 
                 lanes.append((s, x, attn, buf, v))
         for layer in self._layers():
-            for s, x, attn, buf, _ in lanes:
+            for s, x, attn, buf, v in lanes:
                 with torch.cuda.stream(s):
-                    self._block(x, layer, attn, buf, cap)
+                    self._block(x, layer, attn, buf, (v["pos"], v["slot"]), cap)
         for s, x, _, buf, v in lanes:
             with torch.cuda.stream(s):
                 h = ops.rmsnorm(x, self.w("final_norm"), a.rms_eps, out=buf["h"])

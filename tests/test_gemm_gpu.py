@@ -126,11 +126,8 @@ def test_gemm_split_k(cuda, mode, splits, M, N, K, bn):
     ref = _ref(a, w)
     assert (out.float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item() + 1e-2
     assert torch.equal(out, out2), "split-K reduction must be deterministic"
-    # tile counters (the workspace head) left zero: self-resetting
-    mc = 2 if (mode == "2sm" and M > 128) else 1
-    tiles = -(-M // (128 * mc)) * mc * -(-N // bn)
-    head = (tiles * 16 + 255) // 256 * 256
-    assert int(ws[:head].view(torch.int32).abs().sum()) == 0
+    # the fixed 64 KiB tile-counter head of the workspace is left zero
+    assert int(ws[: 64 << 10].view(torch.int32).abs().sum()) == 0
     r = torch.randn(M, N, device=cuda, generator=g).to(torch.bfloat16)
     exp = ref + r.float()
     ops.gemm(a, w, out=r, residual=r, block_n=flag, workspace=ws)
@@ -167,3 +164,24 @@ def test_gemm_auto_plan(cuda, M, N, K):
     ref = _ref(a, w)
     assert (out.float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item() + 1e-2, plan
     assert torch.equal(out, out2)
+
+
+def test_gemm_split_k_shared_workspace_sequence(cuda):
+    """Many split-K GEMMs of different tile counts through ONE workspace (as
+    a decode step does): the counter area must stay valid across shapes (a
+    layout whose counter area grew with the tile count let one launch's
+    partials masquerade as the next launch's counters)."""
+    from paper_2503_06433_b200._lib import SSB_GEMM_SPLIT_SHIFT
+
+    ws = _ws(cuda)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    shapes = [(96, 10240, 2048, 128, 5), (96, 57344, 1024, 128, 2), (1, 10240, 2048, 128, 5),
+              (200, 8192, 4096, 224, 2), (3, 20480, 1024, 256, 3), (96, 10240, 2048, 128, 5)]
+    for M, N, K, bn, sp in shapes * 2:
+        a = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+        w = (torch.randn(N, K, device=cuda, generator=g) / K**0.5).to(torch.bfloat16)
+        out = ops.gemm(a, w, block_n=bn | (sp << SSB_GEMM_SPLIT_SHIFT), workspace=ws)
+        torch.cuda.synchronize()
+        ref = _ref(a, w)
+        assert (out.float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item() + 1e-2, (M, N, K, bn, sp)
+        assert int(ws[: 64 << 10].view(torch.int32).abs().sum()) == 0

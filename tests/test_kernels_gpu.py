@@ -92,6 +92,76 @@ def test_rope_and_paged_append(cuda):
         assert torch.equal(P[b, 2, 1, :, o], qkv.view(T, -1, d)[t, nq + nk :])
 
 
+@pytest.mark.parametrize("flag", ["auto", "b128", "b256_2sm", "split3", "split3_2sm"])
+@pytest.mark.parametrize("M,nq,nk,K,neg", [(300, 8, 2, 512, False), (512, 32, 8, 4096, False),
+                                           (129, 4, 1, 1024, True), (64, 32, 8, 256, True)])
+def test_qkv_gemm_rope_kv_fused_bit_exact(cuda, M, nq, nk, K, neg, flag):
+    """The QKV GEMM with RoPE + paged K/V append in its epilogue equals the
+    unfused gemm -> rope_kv_append pair bit for bit (qkv buffer and pool),
+    for every tile/cluster/split configuration."""
+    from paper_2503_06433_b200._lib import SSB_GEMM_2SM, SSB_GEMM_SPLIT_SHIFT
+
+    bn = {"auto": 0, "b128": 128, "b256_2sm": 256 | SSB_GEMM_2SM, "split3": 128 | (3 << SSB_GEMM_SPLIT_SHIFT),
+          "split3_2sm": 256 | SSB_GEMM_2SM | (3 << SSB_GEMM_SPLIT_SHIFT)}[flag]
+    arch = PRESETS["llama3-8b"]
+    d = 128
+    cos, sin = rope_tables(arch, 2048)
+    tc, ts = torch.from_numpy(cos).to(cuda), torch.from_numpy(sin).to(cuda)
+    g = torch.Generator(device="cuda").manual_seed(M + K)
+    a = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    w = (torch.randn((nq + 2 * nk) * d, K, device=cuda, generator=g) / K**0.5).to(torch.bfloat16)
+    pos = torch.randint(0, 2000, (M,), dtype=torch.int32, device=cuda, generator=g)
+    L, BS = 3, 64
+    NB = -(-M // BS) + 3
+    perm = torch.randperm(NB * BS, device=cuda, generator=g)[:M]
+    slots = perm.to(torch.int64)
+    if neg:
+        slots[::7] = -1
+    geo = (L, nk, BS, d)
+    ws = torch.zeros(64 << 20, dtype=torch.uint8, device=cuda)
+    pool_a = torch.zeros(NB * L * 2 * nk * BS * d, dtype=torch.bfloat16, device=cuda)
+    pool_b = torch.zeros_like(pool_a)
+    if flag == "auto":  # the unfused reference runs the plan the fused launch picks (same fp32 sums)
+        from paper_2503_06433_b200._lib import SSB_EPI_ROPE_KV
+
+        (mode, pbn, sp), _ = ops.gemm_plan(M, w.shape[0], K, SSB_EPI_ROPE_KV, 0, ws.numel())
+        ref_bn = pbn | (SSB_GEMM_2SM if mode == 2 else 0) | (sp << SSB_GEMM_SPLIT_SHIFT if sp > 1 else 0)
+    else:
+        ref_bn = bn
+    ref = ops.gemm(a, w, workspace=ws, block_n=ref_bn)
+    ops.rope_kv_append(ref, nq, nk, pos, tc, ts, pool_a, geo, 1, slots)
+    got = torch.empty_like(ref)
+    ops.gemm_qkv_rope_kv(a, w, got, nq, nk, pos, tc, ts, pool_b, geo, 1, slots, block_n=bn, workspace=ws)
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
+    assert torch.equal(pool_a, pool_b)
+
+
+@pytest.mark.parametrize("M,N,K", [(512, 16032, 4096), (7, 1000, 256), (300, 128256, 512), (129, 4000, 1024)])
+def test_lm_head_argmax_fused(cuda, M, N, K):
+    """LM head with the argmax in the GEMM epilogue == fp32 logits + argmax_rows
+    (same values, smallest index on ties; duplicated weight rows force ties)."""
+    g = torch.Generator(device="cuda").manual_seed(M * N)
+    h = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=cuda, generator=g) / K**0.5).to(torch.bfloat16)
+    w[N // 2] = w[N // 3]  # exact ties between two columns
+    w[N - 1] = w[5]
+    h[0] = 0  # an all-zero row: every logit ties at 0 -> index 0
+    ws = torch.zeros(64 << 20, dtype=torch.uint8, device=cuda)
+    base = 1000
+    logits = ops.gemm(h, w, out_f32=True, workspace=ws)
+    v_ref = torch.empty(M, dtype=torch.float32, device=cuda)
+    i_ref = torch.empty(M, dtype=torch.int32, device=cuda)
+    ops.argmax_rows(logits, base, v_ref, i_ref)
+    v = torch.empty_like(v_ref)
+    i = torch.empty_like(i_ref)
+    ops.lm_head_argmax(h, w, base, v, i, workspace=ws)
+    torch.cuda.synchronize()
+    assert torch.equal(i, i_ref)
+    assert torch.equal(v, v_ref)
+    assert int(i[0]) == base
+
+
 def test_embedding_vocab_parallel(cuda):
     table = torch.randn(100, 256, device=cuda).to(torch.bfloat16)
     ids = torch.tensor([5, 150, 100, 199, 120], dtype=torch.int32, device=cuda)
@@ -131,9 +201,10 @@ def _attn_ref(q, k, v, causal_offset=None):
     return torch.einsum("hqk,khd->qhd", s.softmax(-1), v)
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1, 2])
 @pytest.mark.parametrize("d,nq,nk,lens", [(128, 8, 2, [1024, 77, 130]), (64, 4, 4, [64, 1, 200]),
-                                          (128, 32, 8, [300]), (128, 4, 4, [128, 129, 1, 255, 256])])
+                                          (128, 32, 8, [300]), (128, 4, 4, [128, 129, 1, 255, 256]),
+                                          (128, 32, 8, [1024] * 6 + [77, 700])])
 def test_prefill_attention(cuda, d, nq, nk, lens, variant):
     T = sum(lens)
     qkv = torch.randn(T, (nq + 2 * nk) * d, device=cuda).to(torch.bfloat16)
