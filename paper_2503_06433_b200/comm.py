@@ -97,7 +97,11 @@ class SoloComm(Comm):
 
 
 class TorchComm(Comm):
-    """torch.distributed process group (NCCL on GPU, gloo on CPU)."""
+    """torch.distributed process group: NCCL on the GPU boxes (one process
+    per GPU).  With the gloo backend, CUDA tensors are staged through host
+    memory — the path the multi-process tests use to run the real SPMD engine
+    as several processes on the single GPU a test box has; it is never the
+    data path of a multi-GPU run."""
 
     def __init__(self, group=None, ranks: Sequence[int] | None = None) -> None:
         import torch.distributed as dist
@@ -107,24 +111,44 @@ class TorchComm(Comm):
         self.global_ranks = list(ranks) if ranks is not None else list(range(dist.get_world_size()))
         self.size = len(self.global_ranks)
         self.rank = self.global_ranks.index(dist.get_rank())
+        self._host_staged = dist.get_backend(group) == "gloo"
+
+    def _stage(self, t: torch.Tensor) -> torch.Tensor:
+        if self._host_staged and t.is_cuda:
+            return t.detach().cpu()
+        return t
+
+    @staticmethod
+    def _unstage(dst: torch.Tensor, host: torch.Tensor) -> None:
+        if host.data_ptr() != dst.data_ptr():
+            dst.copy_(host)
 
     def all_to_all(self, out, inp, out_splits, in_splits) -> None:
         os_, is_ = [int(x) for x in out_splits], [int(x) for x in in_splits]
         # staging buffers are allocated for the largest chunk: pass exact views
-        self._dist.all_to_all_single(out[: sum(os_)], inp[: sum(is_)], os_, is_, group=self.group)
+        o, i = out[: sum(os_)], inp[: sum(is_)]
+        ho, hi = self._stage(o), self._stage(i)
+        self._dist.all_to_all_single(ho, hi, os_, is_, group=self.group)
+        self._unstage(o, ho)
 
     def all_reduce_(self, t) -> None:
         if self.size > 1:
-            self._dist.all_reduce(t, group=self.group)
+            h = self._stage(t)
+            self._dist.all_reduce(h, group=self.group)
+            self._unstage(t, h)
 
     def all_gather(self, out, inp) -> None:
-        self._dist.all_gather_into_tensor(out, inp.contiguous(), group=self.group)
+        ho = self._stage(out)
+        self._dist.all_gather_into_tensor(ho, self._stage(inp.contiguous()), group=self.group)
+        self._unstage(out, ho)
 
     def send(self, t, dst) -> None:
-        self._dist.send(t, self.global_ranks[dst], group=self.group)
+        self._dist.send(self._stage(t), self.global_ranks[dst], group=self.group)
 
     def recv(self, t, src) -> None:
-        self._dist.recv(t, self.global_ranks[src], group=self.group)
+        h = self._stage(t)
+        self._dist.recv(h, self.global_ranks[src], group=self.group)
+        self._unstage(t, h)
 
     def barrier(self) -> None:
         if self.size > 1:

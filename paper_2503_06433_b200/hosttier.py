@@ -102,6 +102,12 @@ class HostTier:
         pool blocks, both on the copy stream (overlaps decode compute)."""
         L, H, _, _ = geometry
         cs = self.copy_stream
+        # the block-id tensor was allocated on the compute stream but is read
+        # by the scatter kernel on the copy stream: without this the caching
+        # allocator may hand its memory to a compute-stream tensor while the
+        # scatter (queued behind hundreds of MB of H2D) has not run yet, and
+        # the scatter then writes to garbage block ids (seen at 70B scale)
+        blocks.record_stream(cs)
         i = self._take_staging(cs)
         stg = self.staging[i]
         addr, pitch, width, height = self._piece(slot, n_tokens, glayer0, L, ghead0, H)

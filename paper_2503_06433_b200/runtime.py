@@ -127,6 +127,8 @@ class Worker:
         self.fuse_rope = os.environ.get("SSB_FUSE_ROPE", "1") != "0"
         # greedy argmax in the LM-head GEMM epilogue
         self.fuse_argmax = os.environ.get("SSB_FUSE_ARGMAX", "1") != "0"
+        # split-K for skinny projections (a workspace per lane)
+        self.split_k = os.environ.get("SSB_SPLIT_K", "1") != "0"
 
     # ------------------------------------------------------------ layouts --
     def _tp_comm(self, cfg: ParallelismConfig, stage: int) -> Comm:
@@ -354,7 +356,7 @@ class Worker:
             # split-K workspace of this lane's stream (zeroed once; the GEMM
             # leaves its tile counters zero), see ssb_gemm_bf16_ws
             slot["ws"] = torch.zeros(self.GEMM_WS_BYTES, dtype=torch.uint8, device=self.device)
-        slot["buf"]["ws"] = slot["ws"]
+        slot["buf"]["ws"] = slot["ws"] if self.split_k else None
         return slot["buf"]
 
     def _logits_argmax(self, h_last: torch.Tensor, out_tokens: torch.Tensor, ws: torch.Tensor | None = None) -> None:

@@ -1,2 +1,3 @@
-timeout 300 python tools/debug_split.py 2>&1 | grep -c "err=0.0[0-9]"
-timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -4
+timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -3
+bash tools/profile.sh launches
+ls -la gpurun_out/prof/
