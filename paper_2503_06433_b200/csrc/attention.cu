@@ -7,6 +7,9 @@
 // Reference counterparts (analytic only): prefill attention traffic/compute
 // perf.py:68-89/:104-106; decode attention traffic perf.py:87-88 — the term
 // that dominates TP decode.
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "seesaw_b200.h"
 
@@ -428,6 +431,224 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// ------------------------------------------------------------------------
+// Persistent decode attention: 2 CTAs per SM loop over (sequence, KV head)
+// items round-robin.  The TMA producer (thread 0) walks a flattened
+// (item, block) cursor, so while the 4 warps finish item i and merge it, the
+// ring already holds the first blocks of item i+1: no per-CTA prologue or
+// drain gap in the HBM stream (the per-(b, kvh) kernel above reaches ~83 %
+// of DRAM peak in isolation, limited by those gaps).  The 4-warp merge uses
+// its own smem region ([4][G][D] fp32) so it never touches the ring.
+// ------------------------------------------------------------------------
+constexpr int kPStages = 3;
+
+template <int D>
+struct DecodeSmemP {
+  static constexpr int kTile = kBlk * D * 2;
+  static constexpr int kStage = 2 * kTile;
+  static constexpr int kRing = kPStages * kStage;
+  static int bytes(int G) { return kRing + 64 /*barriers*/ + 2 * 4 * 16 * 4 + 4 * G * D * 4 + 1024; }
+};
+
+template <int D>
+__global__ void __launch_bounds__(128)
+    decode_attn_persistent(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* __restrict__ qkv,
+                           int ld, int nq, int nk, const int32_t* __restrict__ block_tables, int max_blocks,
+                           const int32_t* __restrict__ ctx_lens, int B, ssb_kv_geometry geo, int layer,
+                           __nv_bfloat16* __restrict__ out, int ldo, float scale_log2) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  using S = DecodeSmemP<D>;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kRing);
+  uint64_t* empty = full + kPStages;
+  float* sm_m = reinterpret_cast<float*>(smem + S::kRing + 64);  // [4][16]
+  float* sm_l = sm_m + 4 * 16;                                   // [4][16]
+  float* sm_o = sm_l + 4 * 16;                                   // [4][G][D]
+  const int G = nq / nk;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_items = B * nk;
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tmap);
+    for (int st = 0; st < kPStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 4);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // ---- producer cursor (thread 0 only): next (item, block) to load ----
+  int p_item = blockIdx.x, p_blk = 0, p_nblk = 0;
+  uint32_t p_count = 0;  // blocks issued so far (ring slot = p_count % kPStages)
+  auto p_seek = [&]() {  // skip to an item with blocks left
+    while (p_item < n_items) {
+      if (p_blk == 0) p_nblk = (ctx_lens[p_item / nk] + kBlk - 1) / kBlk;
+      if (p_blk < p_nblk) return true;
+      p_item += gridDim.x;
+      p_blk = 0;
+    }
+    return false;
+  };
+  auto issue_next = [&]() {
+    if (!p_seek()) return;
+    const int st = p_count % kPStages;
+    const int b = p_item / nk, kvh = p_item - (p_item / nk) * nk;
+    const int64_t blk = block_tables[static_cast<size_t>(b) * max_blocks + p_blk];
+    const int row_k = static_cast<int>((((blk * geo.n_layers + layer) * 2 + 0) * geo.n_heads + kvh) * kBlk);
+    const int row_v = static_cast<int>((((blk * geo.n_layers + layer) * 2 + 1) * geo.n_heads + kvh) * kBlk);
+    uint8_t* kt = smem + st * S::kStage;
+    uint8_t* vt = kt + S::kTile;
+    mbar_arrive_expect_tx(&full[st], S::kStage);
+#pragma unroll
+    for (int sub = 0; sub < D / 64; ++sub) {
+      tma_load_2d(kt + sub * kBlk * 128, &tmap, &full[st], sub * 64, row_k, policy_evict_first());
+      tma_load_2d(vt + sub * kBlk * 128, &tmap, &full[st], sub * 64, row_v, policy_evict_first());
+    }
+    ++p_count;
+    ++p_blk;
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kPStages; ++i) issue_next();
+
+  uint32_t c_count = 0;  // blocks consumed so far
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int b = item / nk, kvh = item - (item / nk) * nk;
+    const int ctx = ctx_lens[b];
+    const int nblk = (ctx + kBlk - 1) / kBlk;
+    uint32_t qf[D / 16][4];
+    {
+      const int r0 = lane >> 2, r1 = r0 + 8;
+      const __nv_bfloat16* q = qkv + static_cast<size_t>(b) * ld + static_cast<size_t>(kvh) * G * D;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const int c = kk * 16 + (lane & 3) * 2;
+        qf[kk][0] = r0 < G ? *reinterpret_cast<const uint32_t*>(q + r0 * D + c) : 0u;
+        qf[kk][1] = r1 < G ? *reinterpret_cast<const uint32_t*>(q + r1 * D + c) : 0u;
+        qf[kk][2] = r0 < G ? *reinterpret_cast<const uint32_t*>(q + r0 * D + c + 8) : 0u;
+        qf[kk][3] = r1 < G ? *reinterpret_cast<const uint32_t*>(q + r1 * D + c + 8) : 0u;
+      }
+    }
+    float o[D / 8][4];
+#pragma unroll
+    for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
+
+    for (int j = 0; j < nblk; ++j, ++c_count) {
+      const int st = c_count % kPStages;
+      const uint32_t parity = (c_count / kPStages) & 1;
+      mbar_wait(&full[st], parity);
+      const uint32_t kt = smem_u32(smem + st * S::kStage);
+      const uint32_t vt = kt + S::kTile;
+      float sc[2][4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) sc[i][0] = sc[i][1] = sc[i][2] = sc[i][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        uint32_t b0, b1, b2, b3;
+        const int n = warp * 16 + (lane & 7) + ((lane >> 4) << 3);
+        const int k = kk * 16 + ((lane >> 3) & 1) * 8;
+        ldsm_x4(kt + swz(n, k, kBlk), b0, b1, b2, b3);
+        mma16816(sc[0], qf[kk], b0, b1);
+        mma16816(sc[1], qf[kk], b2, b3);
+      }
+      const int kv0 = j * kBlk + warp * 16;
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int kv = kv0 + i * 8 + (lane & 3) * 2 + (e & 1);
+          sc[i][e] = kv < ctx ? sc[i][e] * scale_log2 : -INFINITY;
+        }
+      float corr[2];
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+        float mx = fmaxf(fmaxf(sc[0][2 * hr], sc[0][2 * hr + 1]), fmaxf(sc[1][2 * hr], sc[1][2 * hr + 1]));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float m_new = fmaxf(m_r[hr], mx);
+        const float m_use = m_new == -INFINITY ? 0.f : m_new;
+        corr[hr] = exp2f(m_r[hr] - m_use);
+        m_r[hr] = m_new;
+        float sum = 0.f;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          sc[i][2 * hr] = exp2f(sc[i][2 * hr] - m_use);
+          sc[i][2 * hr + 1] = exp2f(sc[i][2 * hr + 1] - m_use);
+          sum += sc[i][2 * hr] + sc[i][2 * hr + 1];
+        }
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        l_r[hr] = l_r[hr] * corr[hr] + sum;
+      }
+#pragma unroll
+      for (int i = 0; i < D / 8; ++i) {
+        o[i][0] *= corr[0];
+        o[i][1] *= corr[0];
+        o[i][2] *= corr[1];
+        o[i][3] *= corr[1];
+      }
+      uint32_t a[4];
+      a[0] = pack_bf16x2(sc[0][0], sc[0][1]);
+      a[1] = pack_bf16x2(sc[0][2], sc[0][3]);
+      a[2] = pack_bf16x2(sc[1][0], sc[1][1]);
+      a[3] = pack_bf16x2(sc[1][2], sc[1][3]);
+#pragma unroll
+      for (int dp = 0; dp < D / 16; ++dp) {
+        uint32_t b0, b1, b2, b3;
+        const int t = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        const int c = dp * 16 + (lane >> 4) * 8;
+        ldsm_x4_t(vt + swz(t, c, kBlk), b0, b1, b2, b3);
+        mma16816(o[2 * dp], a, b0, b1);
+        mma16816(o[2 * dp + 1], a, b2, b3);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (threadIdx.x == 0) {
+        mbar_wait(&empty[st], parity);
+        issue_next();  // possibly the first blocks of this CTA's next item
+      }
+    }
+    // merge the 4 warps' partial states (rows < G are real) in the merge region
+    const int r0 = lane >> 2, r1 = r0 + 8;
+    if ((lane & 3) == 0) {
+      sm_m[warp * 16 + r0] = m_r[0];
+      sm_m[warp * 16 + r1] = m_r[1];
+      sm_l[warp * 16 + r0] = l_r[0];
+      sm_l[warp * 16 + r1] = l_r[1];
+    }
+#pragma unroll
+    for (int i = 0; i < D / 8; ++i) {
+      const int c = i * 8 + (lane & 3) * 2;
+      if (r0 < G) {
+        sm_o[(warp * G + r0) * D + c] = o[i][0];
+        sm_o[(warp * G + r0) * D + c + 1] = o[i][1];
+      }
+      if (r1 < G) {
+        sm_o[(warp * G + r1) * D + c] = o[i][2];
+        sm_o[(warp * G + r1) * D + c + 1] = o[i][3];
+      }
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
+      const int r = idx / D, c = idx - r * D;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) M = fmaxf(M, sm_m[w * 16 + r]);
+      const float Mu = M == -INFINITY ? 0.f : M;
+      float L = 0.f, acc = 0.f;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const float f = exp2f(sm_m[w * 16 + r] - Mu);
+        L += sm_l[w * 16 + r] * f;
+        acc += sm_o[(w * G + r) * D + c] * f;
+      }
+      out[static_cast<size_t>(b) * ldo + (kvh * G + r) * D + c] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
+    }
+    __syncthreads();  // the merge region is rewritten by the next item
+  }
+}
+
 template <int D>
 int launch_prefill(const void* qkv, int ld, int nq, int nk, const int32_t* cu, int nseq, int max_len,
                    void* out, int ldo, float scale, cudaStream_t s) {
@@ -457,6 +678,27 @@ int launch_decode(const void* qkv, int ld, int nq, int nk, const void* pool, ssb
   }
   int rc = encode_tmap_2d_bf16(&map, pool, D, rows, D * 2, 64, 64);
   if (rc) return rc;
+  static const int variant = [] {
+    const char* e = getenv("SSB_DECODE_ATTN_VARIANT");  // A/B: 1 = one CTA per (sequence, KV head)
+    return e ? atoi(e) : 0;
+  }();
+  if (variant == 0) {
+    const int G = nq / nk;
+    const int smem = DecodeSmemP<D>::bytes(G);
+    static int attr_p = 0;
+    if (attr_p < smem) {
+      SSB_CUDA(cudaFuncSetAttribute(decode_attn_persistent<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr_p = smem;
+    }
+    int per_sm = 0;
+    SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_attn_persistent<D>, 128, smem));
+    const long items = static_cast<long>(B) * nk;
+    const int grid = static_cast<int>(std::min<long>(items, static_cast<long>(std::max(per_sm, 1)) * num_sms()));
+    decode_attn_persistent<D><<<grid, 128, smem, s>>>(map, static_cast<const __nv_bfloat16*>(qkv), ld, nq, nk, tables,
+                                                     max_blocks, ctx, B, geo, layer, static_cast<__nv_bfloat16*>(out),
+                                                     ldo, scale * kLog2e);
+    return check_launch("decode_attn_persistent");
+  }
   static bool attr = false;
   if (!attr) {
     SSB_CUDA(cudaFuncSetAttribute(decode_attn_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,

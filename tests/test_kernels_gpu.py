@@ -222,7 +222,11 @@ def test_prefill_attention(cuda, d, nq, nk, lens, variant):
 
 
 @pytest.mark.parametrize("d,nq,nk,ctxs", [(128, 32, 8, [1, 64, 65, 1000, 1280]), (64, 4, 4, [96, 7, 128]),
-                                          (128, 4, 1, [500, 33])])
+                                          (128, 4, 1, [500, 33]),
+                                          # more (sequence, KV head) items than resident CTAs: the
+                                          # persistent kernel's ring carries blocks across items
+                                          (128, 32, 8, list(np.random.default_rng(3).integers(1, 400, 90))),
+                                          (128, 8, 1, [1] * 700 + [65, 130])])
 def test_decode_attention_paged(cuda, d, nq, nk, ctxs):
     B, L, BS = len(ctxs), 2, 64
     nblk = [-(-c // BS) for c in ctxs]

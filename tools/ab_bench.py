@@ -23,6 +23,8 @@ def main() -> None:
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--prompts", type=int, default=512)
     ap.add_argument("--output-len", type=int, default=256)
+    ap.add_argument("--configs", default="base,no_rope_fusion,no_argmax_fusion,no_split_k,attn_per_tile_ctas")
+    ap.add_argument("--tag", default="")
     args = ap.parse_args()
     from paper_2503_06433_b200 import PRESETS, ParallelismConfig, Request, SchedulingPolicy, execute, ops
     from paper_2503_06433_b200.comm import SoloComm
@@ -55,7 +57,7 @@ def main() -> None:
         torch.cuda.synchronize()
         return s.elapsed_time(e) / 1e3, rep
 
-    names = ["base", "no_rope_fusion", "no_argmax_fusion", "no_split_k", "attn_per_tile_ctas"]
+    names = args.configs.split(",")
     setc("base")
     batch()
     batch()
@@ -68,7 +70,7 @@ def main() -> None:
     base = sum(r["s"] for r in res["base"]) / args.reps
     for n in names:
         m = sum(r["s"] for r in res[n]) / args.reps
-        print(json.dumps({"config": n, "mean_s": m, "vs_base": m / base,
+        print(json.dumps({"tag": args.tag, "config": n, "mean_s": m, "vs_base": m / base,
                           "tokens_per_s": args.prompts * args.output_len / m, "runs": res[n]}), flush=True)
 
 
