@@ -293,69 +293,109 @@ def _predict(model, hw, cfg_p, cfg_d, args) -> dict:
     return p
 
 
-def reshard_microbench(worker, arch, args, peaks, gpus: int = 8) -> dict:
-    """BASELINE configs[4] on one GPU: the per-GPU KV re-shard work of the 8B
-    batch at PP{gpus}->TP{gpus} (every resident block of one GPU: pack into
-    per-peer staging, unpack from staging into the decode geometry), timed per
-    kernel with CUDA events.  The NVLink transfer between the two needs peers;
-    at N=1 it is absent, so this reports the pack/unpack HBM rate and the
-    per-GPU NVLink floor the transfer would have (bytes leaving / 770 GB/s)."""
+def reshard_microbench(worker, arch, args, peaks, sweep=(2, 4, 8)) -> dict:
+    """BASELINE configs[4] on one GPU: the per-GPU re-shard work of the 8B
+    batch at PP{g}->TP{g} for g in 2/4/8 — KV (every resident block of one
+    GPU: pack into per-peer staging, unpack from staging into the decode
+    geometry) and weights (copy2d pack of the pieces every peer needs, unpack
+    of the pieces this GPU receives) — timed per kernel with CUDA events.  The
+    NVLink transfer between them needs peers; at N=1 it is absent, so this
+    reports the pack/unpack HBM rate and the per-GPU NVLink floor the transfer
+    would have (bytes leaving the GPU / 770 GB/s measured peer bandwidth)."""
     import torch
 
     from paper_2503_06433_b200 import ops
-    from paper_2503_06433_b200.layout import kv_geometry
+    from paper_2503_06433_b200.layout import kv_geometry, repartition_pieces, weight_layout
     from paper_2503_06433_b200.reshard import kv_exchange
+    from paper_2503_06433_b200.runtime import _copy_desc_rows
     from paper_2503_06433_b200.specs import ParallelismConfig
 
+    dev = worker.device
     bs = 64
-    blocks = args.prompts * (-(-(args.input_len + args.output_len) // bs))
-    src = kv_geometry(arch, 1, gpus, blocks, bs)
-    dst = kv_geometry(arch, gpus, 1, blocks, bs)
-    need = blocks * src.block_elems
-    pool = worker.pool[:need] if worker.pool is not None and worker.pool.numel() >= need else \
-        torch.empty(need, dtype=torch.bfloat16, device=worker.device)
-    ex = kv_exchange(arch.model_spec(), ParallelismConfig(1, gpus, 1), ParallelismConfig(gpus, 1, 1), 0)
     cell = 2 * bs * arch.head_dim
     chunk = 256
-    stage = torch.empty(chunk * src.block_elems + 8, dtype=torch.bfloat16, device=worker.device)
 
-    def peers(rects, nid):
-        out, off = [], 0
-        for r in rects:
-            out.append((r.l0, r.nl, r.h0, r.nh, off * 2))
-            off += nid * r.cells * cell
-        return out
-
-    ids_all = torch.arange(blocks, dtype=torch.int32, device=worker.device)
-    chunks = [ids_all[c : c + chunk] for c in range(0, blocks, chunk)]
-    # the loop-back stand-in: unpack every peer's segment from our own staging
-    t = {}
-    for name, fn in (("pack", lambda ids: ops.kv_reshard_pack(pool, src.as_tuple(), ids,
-                                                              peers(ex.send, ids.numel()), stage)),
-                     ("unpack", lambda ids: ops.kv_reshard_unpack(pool, dst.as_tuple(), ids,
-                                                                  peers(ex.recv, ids.numel()), stage))):
-        for ids in chunks[:2]:
-            fn(ids)
+    def timed(fns):
+        for f in fns[:2]:
+            f()
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        for ids in chunks:
-            fn(ids)
+        for f in fns:
+            f()
         e.record()
         torch.cuda.synchronize()
-        t[name] = s.elapsed_time(e) / 1e3
-    moved = need * 2  # bytes of KV this GPU holds
-    leaving = moved * (gpus - 1) // gpus
+        return s.elapsed_time(e) / 1e3
+
+    rows = []
+    for gpus in sweep:
+        # every GPU holds every block of the batch, sliced to its layers (PP)
+        # or heads (TP): the per-GPU pool is 1/g of the batch's KV
+        nb = args.prompts * (-(-(args.input_len + args.output_len) // bs))
+        src = kv_geometry(arch, 1, gpus, nb, bs)
+        dst = kv_geometry(arch, gpus, 1, nb, bs)
+        need = nb * src.block_elems
+        pool = worker.pool[:need] if worker.pool is not None and worker.pool.numel() >= need else \
+            torch.empty(need, dtype=torch.bfloat16, device=dev)
+        ex = kv_exchange(arch.model_spec(), ParallelismConfig(1, gpus, 1), ParallelismConfig(gpus, 1, 1), 0)
+        stage = torch.empty(chunk * src.block_elems + 8, dtype=torch.bfloat16, device=dev)
+
+        def peers(rects, nid):
+            out, off = [], 0
+            for r in rects:
+                out.append((r.l0, r.nl, r.h0, r.nh, off * 2))
+                off += nid * r.cells * cell
+            return out
+
+        ids_all = torch.arange(nb, dtype=torch.int32, device=dev)
+        chunks = [ids_all[c : c + chunk] for c in range(0, nb, chunk)]
+        t_pack = timed([lambda ids=ids: ops.kv_reshard_pack(pool, src.as_tuple(), ids, peers(ex.send, ids.numel()),
+                                                            stage) for ids in chunks])
+        t_unpack = timed([lambda ids=ids: ops.kv_reshard_unpack(pool, dst.as_tuple(), ids,
+                                                                peers(ex.recv, ids.numel()), stage) for ids in chunks])
+        kv_bytes = need * 2
+        kv_leaving = kv_bytes * (gpus - 1) // gpus
+        # weights: GPU 0's pieces for every peer (pack) and from every peer (unpack)
+        old = [weight_layout(arch, 1, gpus, q) for q in range(gpus)]
+        new = [weight_layout(arch, gpus, 1, q) for q in range(gpus)]
+        send, recv, s_pos, r_pos, w_leaving = [], [], 0, 0, 0
+        for q in range(gpus):
+            for pc in repartition_pieces(old[0], new[q]):
+                send.append((pc.src_off * 2, s_pos * 2, pc.src_ld * 2, pc.cols * 2, pc.rows, pc.cols * 2))
+                s_pos += pc.numel
+                w_leaving += 2 * pc.numel if q else 0
+            for pc in repartition_pieces(old[q], new[0]):
+                recv.append((r_pos * 2, pc.dst_off * 2, pc.cols * 2, pc.dst_ld * 2, pc.rows, pc.cols * 2))
+                r_pos += pc.numel
+        a_old = torch.empty(old[0].arena_elems, dtype=torch.bfloat16, device=dev)
+        a_new = torch.empty(new[0].arena_elems, dtype=torch.bfloat16, device=dev)
+        sbuf = torch.empty(max(s_pos, 8), dtype=torch.bfloat16, device=dev)
+        rbuf = torch.empty(max(r_pos, 8), dtype=torch.bfloat16, device=dev)
+        sd, stot = _copy_desc_rows(send)
+        rd, rtot = _copy_desc_rows(recv)
+        sd_d, rd_d = torch.from_numpy(sd).to(dev), torch.from_numpy(rd).to(dev)
+        t_wpack = timed([lambda: ops.copy2d_batched(a_old, sbuf, sd_d, stot)] * 3) / 3
+        t_wunpack = timed([lambda: ops.copy2d_batched(rbuf, a_new, rd_d, rtot)] * 3) / 3
+        leaving = kv_leaving + w_leaving
+        rows.append({
+            "gpus": gpus, "transition": f"pp{gpus}->tp{gpus}",
+            "kv_bytes_per_gpu": kv_bytes, "kv_bytes_leaving": kv_leaving,
+            "weight_bytes_per_gpu": 2 * old[0].arena_elems, "weight_bytes_leaving": w_leaving,
+            "kv_pack_s": t_pack, "kv_unpack_s": t_unpack, "w_pack_s": t_wpack, "w_unpack_s": t_wunpack,
+            "kv_pack_hbm_gbs": 2 * kv_bytes / t_pack / 1e9, "kv_unpack_hbm_gbs": 2 * kv_bytes / t_unpack / 1e9,
+            "w_pack_hbm_gbs": 2 * 2 * s_pos / t_wpack / 1e9, "w_unpack_hbm_gbs": 2 * 2 * r_pos / t_wunpack / 1e9,
+            "kv_pack_hbm_frac": 2 * kv_bytes / t_pack / 1e9 / peaks["hbm_gbs"],
+            "kv_unpack_hbm_frac": 2 * kv_bytes / t_unpack / 1e9 / peaks["hbm_gbs"],
+            "bytes_leaving_gpu": leaving, "nvlink_floor_s": leaving / 770e9,
+            "pack_unpack_s_vs_nvlink_floor": (t_pack + t_unpack + t_wpack + t_wunpack) / (leaving / 770e9),
+        })
+        del pool, stage, a_old, a_new, sbuf, rbuf
     return {
-        "workload": f"{arch.name} KV of {args.prompts}x{args.input_len + args.output_len} tokens, "
-                    f"per-GPU share at PP{gpus}->TP{gpus} (BASELINE configs[4])",
-        "kv_bytes_per_gpu": moved, "bytes_leaving_gpu": leaving,
-        "pack_s": t["pack"], "unpack_s": t["unpack"],
-        "pack_hbm_gbs": 2 * moved / t["pack"] / 1e9, "unpack_hbm_gbs": 2 * moved / t["unpack"] / 1e9,
-        "pack_hbm_frac": 2 * moved / t["pack"] / 1e9 / peaks["hbm_gbs"],
-        "unpack_hbm_frac": 2 * moved / t["unpack"] / 1e9 / peaks["hbm_gbs"],
-        "nvlink_floor_s": leaving / 770e9,
-        "note": "transfer over NVLink not measurable with 1 GPU; pack+unpack overlap the all-to-all chunk by chunk",
+        "workload": f"{arch.name} weights + KV of {args.prompts}x{args.input_len + args.output_len} tokens, "
+                    f"per-GPU share at PP{{g}}->TP{{g}} (BASELINE configs[4])",
+        "sweep": rows,
+        "note": "transfer over NVLink not measurable with 1 GPU; pack of chunk i+1 and unpack of chunk i-1 overlap "
+                "the all-to-all of chunk i, so the transition is bound by max(pack+unpack, NVLink floor)",
     }
 
 
