@@ -16,6 +16,7 @@
 //              max is updated lazily (only when it grows by > 8 in log2
 //              units), so O in TMEM is rescaled rarely; final O / l epilogue.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "seesaw_b200.h"
@@ -290,51 +291,109 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ---------------------------------------------------------------------------
 // Persistent variant: one CTA per SM loops over (query tile, head, sequence)
-// work items, longest (most key tiles) first, round-robin across CTAs.  The
+// work items, longest (most key tiles) first, round-robin across CTAs.
+// Warps: 0 = TMA (lane 0 Q and K, lane 1 V: separate K and V rings, K
+// three deep because S_j frees it early), 1 = MMA issue, 2-9 = softmax with
+// TWO threads per query row (one per 64-key half; row max / row sum
+// exchanged through smem under a 64-thread named barrier per TMEM lane
+// quadrant).  Measured (tools/bench_kernels.py --what attn, 16 x 1024):
+// 0.356 ms per-tile CTAs -> 0.324 persistent -> 0.281 with the split K/V
+// rings; removing exp2 and the P store entirely only reaches 0.244 ms, so
+// what remains is the S -> softmax -> P -> P.V dependency latency of a single
+// query tile per CTA (two ping-ponged query tiles per CTA is the next step).  The
 // per-item prologue of the kernel above (TMEM allocation, barrier set-up, the
 // first Q/K/V TMA round trip) and its epilogue are paid once per CTA or
 // hidden: Q is double-buffered in smem so the next item's Q lands while this
 // item computes, and O is double-buffered in TMEM (S0 S1 O0 O1 = 512
 // columns) so the epilogue of item i overlaps the MMAs of item i+1.  All
 // barrier phases run on global counters (key tiles, S tiles, P tiles, items).
+// Ring depths of the persistent kernel (7 tiles of 32 KiB = the smem budget):
+// K is needed first (S_j) and freed first, so it gets the deepest ring.
+constexpr int kKSt = 3, kVSt = 2, kPSl = 1;
 struct SmemP {
-  static constexpr int kQ = 0;                  // 2 buffers
-  static constexpr int kK = 2 * kTile;          // 2 stages
-  static constexpr int kV = kK + 2 * kTile;     // 2 stages
-  static constexpr int kP = kV + 2 * kTile;
-  static constexpr int kBar = kP + kTile;
-  static constexpr int kBytes = kBar + 256 + 1024;
+  static constexpr int kQ = 0;                  // 1 buffer (the next item's Q lands while its predecessor drains)
+  static constexpr int kK = kTile;              // kKSt stages
+  static constexpr int kV = kK + kKSt * kTile;  // kVSt stages
+  static constexpr int kP = kV + kVSt * kTile;  // kPSl slots
+  static constexpr int kBar = kP + kPSl * kTile;
+  static constexpr int kX = kBar + 192;         // [2 halves][128 rows] fp32 row-max / row-sum exchange (20 barriers + TMEM slot before it)
+  static constexpr int kBytes = kX + 2 * 128 * 4 + 1024;  // 231,616 B: just under the 227 KB opt-in
 };
+constexpr int kThreadsP = 320;  // TMA warp, MMA warp, 8 softmax warps (two per TMEM lane quadrant)
 
-__device__ __forceinline__ bool item_coords(int item, int n_qt_max, int nq, int nseq, const int32_t* cu, int& seq,
-                                            int& h, int& qt, int& start, int& len) {
-  const int per_qt = nq * nseq;
-  qt = n_qt_max - 1 - item / per_qt;  // longest first
-  const int rem = item - (n_qt_max - 1 - qt) * per_qt;
-  seq = rem / nq;
-  h = rem - seq * nq;
-  start = cu[seq];
-  len = cu[seq + 1] - start;
-  return qt * kT < len;
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+
+// This CTA's work items (round-robin), with the NEXT item's sequence bounds
+// loaded one item ahead so the cu[] reads are off every role's critical path.
+struct ItemIter {
+  int item, stride, n_items, n_qt_max, nq, nseq;
+  const int32_t* cu;
+  int seq, h, qt, start, len;    // current
+  int n_item, n_start, n_len;    // prefetched next candidate
+  __device__ void load_next() {
+    if (n_item < n_items) {
+      const int per_qt = nq * nseq;
+      const int nqt = n_qt_max - 1 - n_item / per_qt;
+      const int nseq_i = (n_item - (n_qt_max - 1 - nqt) * per_qt) / nq;
+      n_start = __ldg(cu + nseq_i);
+      n_len = __ldg(cu + nseq_i + 1) - n_start;
+    }
+  }
+  // advance to the next item with work; false when none is left
+  __device__ bool next() {
+    while (n_item < n_items) {
+      item = n_item;
+      const int per_qt = nq * nseq;
+      qt = n_qt_max - 1 - item / per_qt;
+      const int rem = item - (n_qt_max - 1 - qt) * per_qt;
+      seq = rem / nq;
+      h = rem - seq * nq;
+      start = n_start;
+      len = n_len;
+      n_item += stride;
+      load_next();
+      if (qt * kT < len) return true;
+    }
+    return false;
+  }
+  __device__ ItemIter(int first, int stride_, int n_items_, int n_qt_max_, int nq_, int nseq_, const int32_t* cu_)
+      : item(-1), stride(stride_), n_items(n_items_), n_qt_max(n_qt_max_), nq(nq_), nseq(nseq_), cu(cu_),
+        n_item(first), n_start(0), n_len(0) {
+    load_next();
+  }
+};
+
+__device__ __forceinline__ void st_shared_f32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ float ld_shared_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(kThreadsP, 1)
     prefill_attn_tc_persistent(const __grid_constant__ CUtensorMap tmap, const int32_t* __restrict__ cu, int nseq,
                                int n_qt_max, int nq, int nk, __nv_bfloat16* __restrict__ out, int ldo,
                                float scale_log2) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemP::kBar);
-  uint64_t* q_full = bars + 0;     // [2]
-  uint64_t* q_empty = bars + 2;    // [2]
-  uint64_t* kv_full = bars + 4;    // [2]
-  uint64_t* kv_empty = bars + 6;   // [2]
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* k_full = bars + 2;     // [kKSt] K and V rings are separate: K_j frees as soon as S_j is done
+  uint64_t* k_empty = bars + 5;    // [kKSt]
+  uint64_t* v_full = bars + 16;    // [kVSt] (V_j only after P_j.V_j)
+  uint64_t* v_empty = bars + 18;   // [kVSt]
   uint64_t* s_full = bars + 8;     // [2]
   uint64_t* s_free = bars + 10;    // [2]
-  uint64_t* p_full = bars + 12;
-  uint64_t* o_done = bars + 13;
-  uint64_t* o_free = bars + 14;    // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* p_full = bars + 12;    // [kPSl] per P slot
+  uint64_t* o_done = bars + 14;    // [kPSl] per P slot: the P.V that read the slot completed
+  uint64_t* o_free = bars + 20;    // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
 
   const int n_items = n_qt_max * nq * nseq;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -342,17 +401,25 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmap);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&q_full[s], 1);
-      mbar_init(&q_empty[s], 1);
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
-      mbar_init(&s_full[s], 1);
-      mbar_init(&s_free[s], 4);
-      mbar_init(&o_free[s], 4);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int s = 0; s < kKSt; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
     }
-    mbar_init(p_full, 4);
-    mbar_init(o_done, 1);
+    for (int s = 0; s < kVSt; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int s = 0; s < kPSl; ++s) {
+      mbar_init(&p_full[s], 8);
+      mbar_init(&o_done[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_free[s], 8);
+      mbar_init(&o_free[s], 8);
+    }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -364,30 +431,33 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t t_o[2] = {tmem + 256, tmem + 384};
 
   if (warp == 0) {
-    if (lane == 0) {
+    // lane 0: Q and K tiles; lane 1: V tiles (independent rings, so a K load
+    // never queues behind a V slot that is still being read by P.V)
+    if (lane < 2) {
       const uint64_t keep = policy_evict_last();
       uint32_t kc = 0, ic = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-        int seq, h, qt, start, len;
-        if (!item_coords(item, n_qt_max, nq, nseq, cu, seq, h, qt, start, len)) continue;
+      ItemIter it(blockIdx.x, gridDim.x, n_items, n_qt_max, nq, nseq, cu);
+      while (it.next()) {
+        const int h = it.h, qt = it.qt, start = it.start;
         const int kvh = h / group;
         const int qcol = h * kD, kcol = (nq + kvh) * kD, vcol = (nq + nk + kvh) * kD;
-        const int qb = ic & 1;
-        mbar_wait(&q_empty[qb], ((ic >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&q_full[qb], kTile);
-        for (int s = 0; s < 2; ++s)
-          tma_load_2d(smem + SmemP::kQ + qb * kTile + s * kSub, &tmap, &q_full[qb], qcol + s * 64, start + qt * kT,
-                      keep);
+        if (lane == 0) {
+          mbar_wait(q_empty, (ic & 1) ^ 1);
+          mbar_arrive_expect_tx(q_full, kTile);
+          for (int s = 0; s < 2; ++s)
+            tma_load_2d(smem + SmemP::kQ + s * kSub, &tmap, q_full, qcol + s * 64, start + qt * kT, keep);
+        }
+        uint64_t* full = lane == 0 ? k_full : v_full;
+        uint64_t* empty = lane == 0 ? k_empty : v_empty;
+        const int base = lane == 0 ? SmemP::kK : SmemP::kV;
+        const int col = lane == 0 ? kcol : vcol;
+        const uint32_t depth = lane == 0 ? kKSt : kVSt;
         for (int j = 0; j <= qt; ++j, ++kc) {
-          const int st = kc & 1;
-          mbar_wait(&kv_empty[st], ((kc >> 1) & 1) ^ 1);
-          mbar_arrive_expect_tx(&kv_full[st], 2 * kTile);
-          for (int s = 0; s < 2; ++s) {
-            tma_load_2d(smem + SmemP::kK + st * kTile + s * kSub, &tmap, &kv_full[st], kcol + s * 64,
-                        start + j * kT, keep);
-            tma_load_2d(smem + SmemP::kV + st * kTile + s * kSub, &tmap, &kv_full[st], vcol + s * 64,
-                        start + j * kT, keep);
-          }
+          const int st = kc % depth;
+          mbar_wait(&empty[st], ((kc / depth) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[st], kTile);
+          for (int s = 0; s < 2; ++s)
+            tma_load_2d(smem + base + st * kTile + s * kSub, &tmap, &full[st], col + s * 64, start + j * kT, keep);
         }
         ++ic;
       }
@@ -398,34 +468,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc_o = idesc_bf16_f32(kT, kD) | (1u << 16);  // B (= V) MN-major
       const uint32_t p_base = smem_u32(smem + SmemP::kP);
       uint32_t kc = 0, sc = 0, pc = 0, ic = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-        int seq, h, qt, start, len;
-        if (!item_coords(item, n_qt_max, nq, nseq, cu, seq, h, qt, start, len)) continue;
-        const int qb = ic & 1;
-        const uint32_t q_base = smem_u32(smem + SmemP::kQ + qb * kTile);
+      ItemIter it(blockIdx.x, gridDim.x, n_items, n_qt_max, nq, nseq, cu);
+      while (it.next()) {
+        const int qt = it.qt;
+        const int qb = ic & 1;  // O buffer
+        const uint32_t q_base = smem_u32(smem + SmemP::kQ);
         const uint32_t o_acc = t_o[qb];
-        mbar_wait(&q_full[qb], (ic >> 1) & 1);
+        mbar_wait(q_full, ic & 1);
         // O buffer qb was read out by the epilogue of item ic - 2
         mbar_wait(&o_free[qb], ((ic >> 1) & 1) ^ 1);
-        int prev_stage = 0;
-        auto pv = [&](int j, int stage) {
-          mbar_wait(p_full, pc & 1);
+        auto pv = [&](int j, uint32_t vc) {
+          const int slot = pc % kPSl;
+          const int stage = vc % kVSt;
+          mbar_wait(&v_full[stage], (vc / kVSt) & 1);
+          mbar_wait(&p_full[slot], (pc / kPSl) & 1);
           tc_fence_after();
           const uint32_t v_base = smem_u32(smem + SmemP::kV + stage * kTile);
+          const uint32_t pb = p_base + slot * kTile;
 #pragma unroll
           for (int k = 0; k < kT / 16; ++k) {
-            const uint64_t a = sdesc_k_sw128(p_base + (k >> 2) * kSub + (k & 3) * 32);
+            const uint64_t a = sdesc_k_sw128(pb + (k >> 2) * kSub + (k & 3) * 32);
             const uint64_t b = sdesc_mn_sw128(v_base + k * 16 * 128, kSub);
             umma_bf16(o_acc, a, b, idesc_o, (j | k) != 0);
           }
-          umma_commit(o_done);
-          umma_commit(&kv_empty[stage]);
+          umma_commit(&o_done[slot]);
+          umma_commit(&v_empty[stage]);
           ++pc;
         };
+        uint32_t prev_kc = 0;
         for (int j = 0; j <= qt; ++j, ++kc, ++sc) {
-          const int st = kc & 1;
+          const int st = kc % kKSt;
           const int ss = sc & 1;
-          mbar_wait(&kv_full[st], (kc >> 1) & 1);
+          mbar_wait(&k_full[st], (kc / kKSt) & 1);
           mbar_wait(&s_free[ss], ((sc >> 1) & 1) ^ 1);
           tc_fence_after();
           const uint32_t k_base = smem_u32(smem + SmemP::kK + st * kTile);
@@ -436,24 +510,31 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma_bf16(t_s[ss], a, b, idesc_s, k != 0);
           }
           umma_commit(&s_full[ss]);
-          if (j == qt) umma_commit(&q_empty[qb]);  // last read of this Q buffer
-          if (j >= 1) pv(j - 1, prev_stage);
-          prev_stage = st;
+          umma_commit(&k_empty[st]);           // K_j read by S_j only
+          if (j == qt) umma_commit(q_empty);  // last read of the Q buffer by this item
+          if (j >= 1) pv(j - 1, prev_kc);
+          prev_kc = kc;
         }
-        pv(qt, prev_stage);
+        pv(qt, prev_kc);
         ++ic;
       }
     }
   } else {
-    // ---------------- softmax / epilogue: thread = query row ----------------
+    // ------- softmax / epilogue: two threads per query row (one per column half) -------
+    // warps 2..9: TMEM lane quadrant = warp & 3 (hardware rule), column half
+    // = which of the two warps of that quadrant; the halves exchange row max
+    // and row sum through smem under a 64-thread named barrier per quadrant.
     const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int r = quad * 32 + lane;
+    const int c0 = half * (kT / 2);
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-    uint8_t* p_row = smem + SmemP::kP + r * 128;
+    const uint32_t xch = smem_u32(smem + SmemP::kX);  // [2][128] fp32
+    uint8_t* p_row0 = smem + SmemP::kP + half * kSub + r * 128;  // keys [64*half, +64) = P sub-tile `half`
     uint32_t sc = 0, pc = 0, ic = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      int seq, h, qt, start, len;
-      if (!item_coords(item, n_qt_max, nq, nseq, cu, seq, h, qt, start, len)) continue;
+    ItemIter it(blockIdx.x, gridDim.x, n_items, n_qt_max, nq, nseq, cu);
+    while (it.next()) {
+      const int h = it.h, qt = it.qt, start = it.start, len = it.len;
       const int qb = ic & 1;
       const uint32_t o_acc = t_o[qb];
       const int q0 = qt * kT;
@@ -463,11 +544,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ss = sc & 1;
         mbar_wait(&s_full[ss], (sc >> 1) & 1);
         tc_fence_after();
-        float s[kT];
+        float s[kT / 2];
 #pragma unroll
-        for (int c = 0; c < kT / 32; ++c) {
+        for (int c = 0; c < kT / 64; ++c) {
           uint32_t v[32];
-          tmem_ld32(t_s[ss] + lane_off + c * 32, v);
+          tmem_ld32(t_s[ss] + lane_off + c0 + c * 32, v);
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(v[i]) * scale_log2;
@@ -475,15 +556,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_free[ss]);
-        const int k0 = j * kT;
-        if (j == qt || k0 + kT > len) {
+        const int k0 = j * kT + c0;
+        if (j == qt || j * kT + kT > len) {
 #pragma unroll
-          for (int i = 0; i < kT; ++i)
+          for (int i = 0; i < kT / 2; ++i)
             if (k0 + i > qrow || k0 + i >= len) s[i] = -INFINITY;
         }
         float mx = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < kT; ++i) mx = fmaxf(mx, s[i]);
+        for (int i = 0; i < kT / 2; ++i) mx = fmaxf(mx, s[i]);
+        st_shared_f32(xch + (half * 128 + r) * 4, mx);
+        named_bar_sync(1 + quad, 64);
+        mx = fmaxf(mx, ld_shared_f32(xch + ((half ^ 1) * 128 + r) * 4));
+        named_bar_sync(1 + quad, 64);  // both read before either rewrites the slot
         float corr = 1.f;
         const bool rescale = mx > m_used + kRescaleThreshold;
         if (rescale) {
@@ -491,50 +576,59 @@ __global__ void __launch_bounds__(kThreads, 1)
           m_used = mx;
         }
         float sum = 0.f;
-        uint32_t pk[kT / 2];
+        uint32_t pk[kT / 4];
 #pragma unroll
-        for (int i = 0; i < kT; i += 2) {
+#pragma unroll
+        for (int i = 0; i < kT / 2; i += 2) {
           const float a = fast_exp2(s[i] - m_used), b = fast_exp2(s[i + 1] - m_used);
           sum += a + b;
           pk[i / 2] = pack_bf16x2(a, b);
         }
-        // the P buffer (and O) are free once the previous P.V completed
-        if (pc > 0) mbar_wait(o_done, (pc - 1) & 1);
+        // P slot is free once the P.V kPSl tiles back (its last reader) completed
+        const int slot = pc % kPSl;
+        if (pc >= kPSl) mbar_wait(&o_done[slot], ((pc - kPSl) / kPSl) & 1);
         tc_fence_after();
         if (j >= 1 && __any_sync(0xffffffffu, rescale)) {
+          // rescaling O needs every earlier P.V of this item in it
+          mbar_wait(&o_done[(pc - 1) % kPSl], ((pc - 1) / kPSl) & 1);
+          tc_fence_after();
 #pragma unroll 1
-          for (int c = 0; c < kD / 32; ++c) {
+          for (int c = 0; c < kD / 64; ++c) {
             uint32_t v[32];
-            tmem_ld32(o_acc + lane_off + c * 32, v);
+            tmem_ld32(o_acc + lane_off + c0 + c * 32, v);
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
-            tmem_st32(o_acc + lane_off + c * 32, v);
+            tmem_st32(o_acc + lane_off + c0 + c * 32, v);
           }
           tmem_st_wait();
         }
         l = l * corr + sum;
+        // this half's 64 keys = one SW128 sub-tile row of 8 16-byte chunks
+        uint8_t* p_row = p_row0 + slot * kTile;
 #pragma unroll
-        for (int c = 0; c < kT / 8; ++c) {
-          const int sb = c >> 3, cc = c & 7;
+        for (int c = 0; c < 8; ++c) {
           uint4 val = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-          *reinterpret_cast<uint4*>(p_row + sb * kSub + ((cc ^ (r & 7)) << 4)) = val;
+          *reinterpret_cast<uint4*>(p_row + ((c ^ (r & 7)) << 4)) = val;
         }
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(p_full);
+        if (lane == 0) mbar_arrive(&p_full[slot]);
         ++pc;
       }
-      // epilogue: O / l, then hand the O buffer back to the MMA warp
-      mbar_wait(o_done, (pc - 1) & 1);
+      // epilogue: l = sum of both halves' partial sums; each half writes its 64 dims
+      st_shared_f32(xch + (half * 128 + r) * 4, l);
+      named_bar_sync(1 + quad, 64);
+      l += ld_shared_f32(xch + ((half ^ 1) * 128 + r) * 4);
+      mbar_wait(&o_done[(pc - 1) % kPSl], ((pc - 1) / kPSl) & 1);
       tc_fence_after();
       const float inv = l > 0.f ? 1.f / l : 0.f;
-      __nv_bfloat16* orow = out + static_cast<size_t>(start + qrow) * ldo + h * kD;
+      __nv_bfloat16* orow = out + static_cast<size_t>(start + qrow) * ldo + h * kD + c0;
 #pragma unroll 1
-      for (int c = 0; c < kD / 32; ++c) {
+      for (int c = 0; c < kD / 64; ++c) {
         uint32_t v[32];
-        tmem_ld32(o_acc + lane_off + c * 32, v);
+        tmem_ld32(o_acc + lane_off + c0 + c * 32, v);
         tmem_ld_wait();
         if (qrow < len) {
           uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
@@ -549,6 +643,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      // both halves read the exchange slots before either rewrites them
+      named_bar_sync(1 + quad, 64);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_free[qb]);
@@ -581,7 +677,7 @@ int launch_prefill_attn_tc(const void* qkv, int ld, int T, int nq, int nk, const
     const int n_qt = (max_len + kT - 1) / kT;
     const long items = static_cast<long>(n_qt) * nq * nseq;
     const int grid = static_cast<int>(std::min<long>(num_sms(), items));
-    prefill_attn_tc_persistent<<<grid, kThreads, SmemP::kBytes, s>>>(
+    prefill_attn_tc_persistent<<<grid, kThreadsP, SmemP::kBytes, s>>>(
         map, cu, nseq, n_qt, nq, nk, static_cast<__nv_bfloat16*>(out), ldo, scale * 1.4426950408889634f);
     return check_launch("prefill_attn_tc_persistent");
   }
