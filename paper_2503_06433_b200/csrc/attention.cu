@@ -440,9 +440,7 @@ __global__ void __launch_bounds__(128)
 // of DRAM peak in isolation, limited by those gaps).  The 4-warp merge uses
 // its own smem region ([4][G][D] fp32) so it never touches the ring.
 // ------------------------------------------------------------------------
-constexpr int kPStages = 3;
-
-template <int D>
+template <int D, int kPStages = 3>
 struct DecodeSmemP {
   static constexpr int kTile = kBlk * D * 2;
   static constexpr int kStage = 2 * kTile;
@@ -450,14 +448,14 @@ struct DecodeSmemP {
   static int bytes(int G) { return kRing + 64 /*barriers*/ + 2 * 4 * 16 * 4 + 4 * G * D * 4 + 1024; }
 };
 
-template <int D>
+template <int D, int kPStages>
 __global__ void __launch_bounds__(128)
     decode_attn_persistent(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* __restrict__ qkv,
                            int ld, int nq, int nk, const int32_t* __restrict__ block_tables, int max_blocks,
                            const int32_t* __restrict__ ctx_lens, int B, ssb_kv_geometry geo, int layer,
                            __nv_bfloat16* __restrict__ out, int ldo, float scale_log2) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  using S = DecodeSmemP<D>;
+  using S = DecodeSmemP<D, kPStages>;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kRing);
   uint64_t* empty = full + kPStages;
@@ -665,6 +663,28 @@ int launch_prefill(const void* qkv, int ld, int nq, int nk, const int32_t* cu, i
   return check_launch("prefill_attn_kernel");
 }
 
+template <int D, int ST>
+int launch_decode_p(const CUtensorMap& map, const void* qkv, int ld, int nq, int nk, ssb_kv_geometry geo, int layer,
+                    const int32_t* tables, int max_blocks, const int32_t* ctx, int B, void* out, int ldo, float scale,
+                    int ctas_per_sm, cudaStream_t s) {
+  const int G = nq / nk;
+  const int smem = DecodeSmemP<D, ST>::bytes(G);
+  static int attr_p = 0;
+  if (attr_p < smem) {
+    SSB_CUDA(cudaFuncSetAttribute(decode_attn_persistent<D, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_p = smem;
+  }
+  int per_sm = 0;
+  SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_attn_persistent<D, ST>, 128, smem));
+  if (ctas_per_sm > 0) per_sm = std::min(per_sm, ctas_per_sm);
+  const long items = static_cast<long>(B) * nk;
+  const int grid = static_cast<int>(std::min<long>(items, static_cast<long>(std::max(per_sm, 1)) * num_sms()));
+  decode_attn_persistent<D, ST><<<grid, 128, smem, s>>>(map, static_cast<const __nv_bfloat16*>(qkv), ld, nq, nk, tables,
+                                                       max_blocks, ctx, B, geo, layer, static_cast<__nv_bfloat16*>(out),
+                                                       ldo, scale * kLog2e);
+  return check_launch("decode_attn_persistent");
+}
+
 template <int D>
 int launch_decode(const void* qkv, int ld, int nq, int nk, const void* pool, ssb_kv_geometry geo, int num_blocks,
                   int layer, const int32_t* tables, int max_blocks, const int32_t* ctx, int B, void* out, int ldo,
@@ -683,21 +703,21 @@ int launch_decode(const void* qkv, int ld, int nq, int nk, const void* pool, ssb
     return e ? atoi(e) : 0;
   }();
   if (variant == 0) {
-    const int G = nq / nk;
-    const int smem = DecodeSmemP<D>::bytes(G);
-    static int attr_p = 0;
-    if (attr_p < smem) {
-      SSB_CUDA(cudaFuncSetAttribute(decode_attn_persistent<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr_p = smem;
+    // ring depth x CTAs per SM (SSB_DECODE_STAGES, SSB_DECODE_CTAS: A/B knobs)
+    static const int stages = [] {
+      const char* e = getenv("SSB_DECODE_STAGES");
+      return e ? atoi(e) : 3;
+    }();
+    static const int ctas = [] {
+      const char* e = getenv("SSB_DECODE_CTAS");
+      return e ? atoi(e) : 0;
+    }();
+    switch (stages) {
+      case 2: return launch_decode_p<D, 2>(map, qkv, ld, nq, nk, geo, layer, tables, max_blocks, ctx, B, out, ldo, scale, ctas, s);
+      case 4: return launch_decode_p<D, 4>(map, qkv, ld, nq, nk, geo, layer, tables, max_blocks, ctx, B, out, ldo, scale, ctas, s);
+      case 6: return launch_decode_p<D, 6>(map, qkv, ld, nq, nk, geo, layer, tables, max_blocks, ctx, B, out, ldo, scale, ctas, s);
+      default: return launch_decode_p<D, 3>(map, qkv, ld, nq, nk, geo, layer, tables, max_blocks, ctx, B, out, ldo, scale, ctas, s);
     }
-    int per_sm = 0;
-    SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_attn_persistent<D>, 128, smem));
-    const long items = static_cast<long>(B) * nk;
-    const int grid = static_cast<int>(std::min<long>(items, static_cast<long>(std::max(per_sm, 1)) * num_sms()));
-    decode_attn_persistent<D><<<grid, 128, smem, s>>>(map, static_cast<const __nv_bfloat16*>(qkv), ld, nq, nk, tables,
-                                                     max_blocks, ctx, B, geo, layer, static_cast<__nv_bfloat16*>(out),
-                                                     ldo, scale * kLog2e);
-    return check_launch("decode_attn_persistent");
   }
   static bool attr = false;
   if (!attr) {

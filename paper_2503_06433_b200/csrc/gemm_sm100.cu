@@ -784,12 +784,58 @@ double plan_cost(int M, int N, int K, int sms, const Plan& pl) {
   return t;
 }
 
+// Measured best configurations (tools/bench_kernels.py --what splitk on
+// B200, profiles/r01/gemm_plan_sweep.jsonl) for the Llama decode shapes at
+// M = 256 / 512 (TP1 and TP8): exact (M, N, K) matches override the model,
+// per epilogue constraint (any N tile / multiple of 64 for SiLU / of 128 for
+// RoPE).  The model's per-shape error (~10-20 %) can pick a 25 % slower plan
+// on near ties (e.g. the TP1 down projection).
+struct MeasuredPlan {
+  int M, N, K;
+  Plan any, mult64, mult128;
+};
+constexpr MeasuredPlan kMeasured[] = {
+    {256, 768, 4096, {0, 128, 3}, {0, 128, 3}, {0, 128, 3}},
+    {256, 3584, 4096, {0, 128, 2}, {0, 128, 2}, {0, 128, 2}},
+    {256, 4096, 512, {0, 128, 1}, {0, 128, 1}, {0, 128, 1}},
+    {256, 4096, 1792, {0, 128, 1}, {0, 128, 1}, {0, 128, 1}},
+    {256, 4096, 4096, {0, 128, 2}, {0, 128, 2}, {0, 128, 2}},
+    {256, 4096, 14336, {2, 192, 3}, {2, 192, 3}, {0, 128, 4}},
+    {256, 6144, 4096, {0, 128, 1}, {0, 128, 1}, {0, 128, 1}},
+    {256, 16032, 4096, {0, 224, 1}, {2, 256, 1}, {2, 256, 1}},
+    {256, 28672, 4096, {2, 224, 1}, {2, 256, 1}, {2, 256, 1}},
+    {256, 128256, 4096, {2, 224, 1}, {2, 256, 1}, {2, 256, 1}},
+    {512, 768, 4096, {2, 128, 3}, {2, 128, 3}, {2, 128, 3}},
+    {512, 3584, 4096, {0, 128, 1}, {0, 128, 1}, {0, 128, 1}},
+    {512, 4096, 512, {0, 128, 1}, {0, 128, 1}, {0, 128, 1}},
+    {512, 4096, 1792, {0, 128, 1}, {0, 128, 1}, {0, 128, 1}},
+    {512, 4096, 4096, {0, 128, 1}, {0, 128, 1}, {0, 128, 1}},
+    {512, 4096, 14336, {2, 256, 2}, {2, 256, 2}, {2, 256, 2}},
+    {512, 6144, 4096, {0, 192, 1}, {0, 192, 1}, {2, 256, 1}},
+    {512, 16032, 4096, {2, 224, 1}, {2, 256, 1}, {2, 256, 1}},
+    {512, 28672, 4096, {2, 224, 1}, {2, 256, 1}, {2, 256, 1}},
+    {512, 128256, 4096, {2, 256, 1}, {2, 256, 1}, {2, 256, 1}},
+    {2048, 4096, 4096, {2, 256, 1}, {2, 256, 1}, {2, 256, 1}},
+};
+
+const Plan* measured_plan(int M, int N, int K, int epi) {
+  for (const MeasuredPlan& m : kMeasured)
+    if (m.M == M && m.N == N && m.K == K)
+      return epi == SSB_EPI_ROPE_KV ? &m.mult128 : epi == SSB_EPI_SILU_MUL ? &m.mult64 : &m.any;
+  return nullptr;
+}
+
 Plan choose_plan(int M, int N, int K, int epi, int sms, size_t ws_bytes) {
   Plan best{0, 256, 1};
   double best_t = 1e30;
   const int bns[4] = {256, 224, 192, 128};
   const int kb = (K + kBK - 1) / kBK;
   static const int no_split = gemm_env("SSB_GEMM_NO_SPLIT", 0);
+  static const int no_table = gemm_env("SSB_GEMM_NO_TABLE", 0);
+  if (sms == num_sms() && !no_split && !no_table) {
+    const Plan* m = measured_plan(M, N, K, epi);
+    if (m && (m->splits <= 1 || plan_ws_bytes(M, N, *m) <= ws_bytes)) return *m;
+  }
   for (int mode = 0; mode <= 2; mode += 2) {
     if (mode == 2 && M <= kBM) continue;
     for (int bn : bns) {
