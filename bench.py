@@ -118,12 +118,21 @@ def run_ours(args) -> None:
     n = args.gpus
     if world != n:
         raise SystemExit(f"--gpus {n} but WORLD_SIZE={world}")
+    # one GPU per rank; ranks beyond the device count share GPUs (gloo test runs)
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        # SSB_DIST_BACKEND=gloo: ranks sharing one GPU (the multi-rank path
+        # exercised on a single-GPU box; TorchComm stages CUDA tensors through
+        # host memory) -- never the measured configuration
+        backend = os.environ.get("SSB_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         comm = TorchComm()
     else:
         comm = SoloComm()
@@ -168,6 +177,8 @@ def run_ours(args) -> None:
         if world > 1:
             import torch.distributed as dist
 
+            if dist.get_backend() == "gloo":
+                t = t.cpu()
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.tolist(), reports
 
@@ -328,7 +339,7 @@ def reshard_microbench(worker, arch, args, peaks, sweep=(2, 4, 8)) -> dict:
         return s.elapsed_time(e) / 1e3
 
     rows = []
-    for gpus in sweep:
+    for gpus in [g for g in sweep if arch.num_layers % g == 0 and arch.num_kv_heads % g == 0]:
         # every GPU holds every block of the batch, sliced to its layers (PP)
         # or heads (TP): the per-GPU pool is 1/g of the batch's KV
         nb = args.prompts * (-(-(args.input_len + args.output_len) // bs))
