@@ -659,6 +659,353 @@ __global__ void __launch_bounds__(kThreadsP, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Pair kernel (GQA group size even): a CTA computes TWO query heads of the
+// same KV group for one 128-row query tile, sharing every K/V tile (128 keys)
+// between them.  P never leaves tensor memory: the softmax writes it (bf16,
+// 64 columns) over the first half of its own S accumulator with tcgen05.st
+// and the P.V MMA reads its A operand from TMEM, so there is no P smem, no
+// proxy fence, and the tensor pipe's in-order execution (P.V(j) is issued
+// before S(j+1) overwrites the aliased columns) replaces the S-buffer barrier.
+// Two softmax warpgroups (one per head, one thread per row) ping-pong with the
+// MMA issuer: while head A turns S_A(j) into P_A(j), the tensor pipe runs
+// P_B(j-1).V and S_B(j) — the S -> softmax -> P -> P.V chain of one head is
+// hidden behind the other head's MMAs.
+// TMEM: S/P_A, S/P_B, O_A, O_B (128 columns each) = 512.
+// smem: Q_A, Q_B 64 KB; K ring 3 x 32 KB, V ring 2 x 32 KB.
+// ---------------------------------------------------------------------------
+constexpr int kPairKSt = 3, kPairVSt = 2;
+// pair i's second exponential by polynomial when (i & kPolyMask): 0 = off.
+// Measured: 1-in-4 on the FMA pipe is 5 % SLOWER (the softmax is issue- not
+// MUFU-bound at 2 warps per SMSP), so every exponential uses ex2.approx.
+constexpr int kPolyMask = 0;
+constexpr int kThreadsPair = 320;
+
+struct SmemPair {
+  static constexpr int kQ = 0;                          // Q_A, Q_B
+  static constexpr int kK = 2 * kTile;                  // kPairKSt x 32 KB
+  static constexpr int kV = kK + kPairKSt * kTile;      // kPairVSt x 32 KB
+  static constexpr int kBar = kV + kPairVSt * kTile;
+  static constexpr int kBytes = kBar + 256 + 1024;
+};
+
+// 2^x on the FMA/ALU pipes (x <= 0): round-to-nearest split via the 1.5*2^23
+// trick, cubic on [-0.5, 0.5] (max rel. error 1.4e-4, far below bf16's 2^-9),
+// exponent added in the integer domain.  Used for a fraction of the softmax
+// exponentials so the MUFU pipe (16 ex2/clk/SM) is not the tile's bottleneck.
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -120.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.05502927f, f, 0.24225698f), f, 0.69325305f), f, 0.99995134f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+}
+
+// D (+)= A . B with A [M=128, K=16] read from TMEM (lane = row, 8 columns of
+// bf16 pairs), B from shared memory.
+__device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                             bool accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate ? 1 : 0));
+}
+
+struct PairIter {
+  int stride, n_items, n_qt_max, pairs, nseq;  // pairs = nq / 2
+  const int32_t* cu;
+  int seq, pair, qt, start, len;
+  int n_item, n_start, n_len;
+  __device__ void load_next() {
+    if (n_item < n_items) {
+      const int per_qt = pairs * nseq;
+      const int q = n_qt_max - 1 - n_item / per_qt;
+      const int sq = (n_item - (n_qt_max - 1 - q) * per_qt) / pairs;
+      n_start = __ldg(cu + sq);
+      n_len = __ldg(cu + sq + 1) - n_start;
+    }
+  }
+  __device__ bool next() {
+    while (n_item < n_items) {
+      const int item = n_item;
+      const int per_qt = pairs * nseq;
+      qt = n_qt_max - 1 - item / per_qt;
+      const int rem = item - (n_qt_max - 1 - qt) * per_qt;
+      seq = rem / pairs;
+      pair = rem - seq * pairs;
+      start = n_start;
+      len = n_len;
+      n_item += stride;
+      load_next();
+      if (qt * kT < len) return true;
+    }
+    return false;
+  }
+  __device__ PairIter(int first, int stride_, int n_items_, int n_qt_max_, int pairs_, int nseq_, const int32_t* cu_)
+      : stride(stride_), n_items(n_items_), n_qt_max(n_qt_max_), pairs(pairs_), nseq(nseq_), cu(cu_), n_item(first),
+        n_start(0), n_len(0) {
+    load_next();
+  }
+};
+
+__global__ void __launch_bounds__(kThreadsPair, 1)
+    prefill_attn_tc_pair(const __grid_constant__ CUtensorMap tmap, const int32_t* __restrict__ cu, int nseq,
+                         int n_qt_max, int nq, int nk, __nv_bfloat16* __restrict__ out, int ldo, float scale_log2) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemPair::kBar);
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* k_full = bars + 2;    // [3]
+  uint64_t* k_empty = bars + 5;   // [3]
+  uint64_t* v_full = bars + 8;    // [2]
+  uint64_t* v_empty = bars + 10;  // [2]
+  uint64_t* s_full = bars + 12;   // [head]: S(t) of the head is in TMEM (and every earlier P.V done)
+  uint64_t* p_full = bars + 14;   // [head]: P(t) written over S(t)
+  uint64_t* o_done = bars + 16;   // [head]: the item's last P.V completed
+  uint64_t* o_free = bars + 18;   // [head]: the epilogue read O
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+
+  const int pairs = nq / 2;
+  const int group = nq / nk;
+  const int n_items = n_qt_max * pairs * nseq;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tmap);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int i = 0; i < kPairKSt; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < kPairVSt; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&o_done[i], 1);
+      mbar_init(&o_free[i], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // columns: S/P of head h at 128 h, O of head h at 256 + 128 h
+  auto t_s = [&](int head) { return tmem + 128u * head; };
+  auto t_o = [&](int head) { return tmem + 256u + 128u * head; };
+
+  if (warp == 0) {
+    // lane 0: Q_A, Q_B and K tiles; lane 1: V tiles
+    if (lane < 2) {
+      const uint64_t keep = policy_evict_last();
+      uint32_t t = 0, ic = 0;
+      PairIter it(blockIdx.x, gridDim.x, n_items, n_qt_max, pairs, nseq, cu);
+      while (it.next()) {
+        const int hA = 2 * it.pair;
+        const int kvh = hA / group;
+        const int n_kv = it.qt + 1;
+        if (lane == 0) {
+          mbar_wait(q_empty, (ic & 1) ^ 1);
+          mbar_arrive_expect_tx(q_full, 2 * kTile);
+          for (int hh = 0; hh < 2; ++hh)
+            for (int sb = 0; sb < 2; ++sb)
+              tma_load_2d(smem + SmemPair::kQ + hh * kTile + sb * kSub, &tmap, q_full, (hA + hh) * kD + sb * 64,
+                          it.start + it.qt * kT, keep);
+        }
+        uint64_t* full = lane == 0 ? k_full : v_full;
+        uint64_t* empty = lane == 0 ? k_empty : v_empty;
+        const int base = lane == 0 ? SmemPair::kK : SmemPair::kV;
+        const uint32_t depth = lane == 0 ? kPairKSt : kPairVSt;
+        const int col = (lane == 0 ? nq + kvh : nq + nk + kvh) * kD;
+        for (int j = 0; j < n_kv; ++j, ++t) {
+          const int st = t % depth;
+          mbar_wait(&empty[st], ((t / depth) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[st], kTile);
+          for (int sb = 0; sb < 2; ++sb)
+            tma_load_2d(smem + base + st * kTile + sb * kSub, &tmap, &full[st], col + sb * 64, it.start + j * kT,
+                        keep);
+        }
+        ++ic;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(kT, kT);
+      constexpr uint32_t idesc_o = idesc_bf16_f32(kT, kD) | (1u << 16);  // B (= V) MN-major
+      uint32_t t = 0, ic = 0;
+      PairIter it(blockIdx.x, gridDim.x, n_items, n_qt_max, pairs, nseq, cu);
+      auto pv = [&](int hh, uint32_t tt, bool first) {
+        // P(tt) of head hh (over its S columns) . V(tt) -> O
+        if (first) mbar_wait(&o_free[hh], (ic & 1) ^ 1);  // the previous item's epilogue read O
+        mbar_wait(&p_full[hh], tt & 1);
+        tc_fence_after();
+        const uint32_t v_base = smem_u32(smem + SmemPair::kV + (tt % kPairVSt) * kTile);
+#pragma unroll
+        for (int k = 0; k < kT / 16; ++k) {
+          const uint64_t b = sdesc_mn_sw128(v_base + k * 16 * 128, kSub);
+          umma_bf16_ts(t_o(hh), t_s(hh) + 8 * k, b, idesc_o, !(first && k == 0));
+        }
+      };
+      while (it.next()) {
+        const int n_kv = it.qt + 1;
+        mbar_wait(q_full, ic & 1);
+        tc_fence_after();
+        const uint32_t q_base = smem_u32(smem + SmemPair::kQ);
+        for (int j = 0; j < n_kv; ++j, ++t) {
+          const int kst = t % kPairKSt;
+          mbar_wait(&k_full[kst], (t / kPairKSt) & 1);
+          if (j >= 1) mbar_wait(&v_full[(t - 1) % kPairVSt], ((t - 1) / kPairVSt) & 1);
+          tc_fence_after();
+          const uint32_t k_base = smem_u32(smem + SmemPair::kK + kst * kTile);
+          for (int hh = 0; hh < 2; ++hh) {
+            if (j >= 1) pv(hh, t - 1, j == 1);  // reads P(t-1) before S(t) overwrites it
+            const uint32_t qa = q_base + hh * kTile;
+#pragma unroll
+            for (int k = 0; k < kD / 16; ++k) {
+              const uint64_t a = sdesc_k_sw128(qa + (k >> 2) * kSub + (k & 3) * 32);
+              const uint64_t b = sdesc_k_sw128(k_base + (k >> 2) * kSub + (k & 3) * 32);
+              umma_bf16(t_s(hh), a, b, idesc_s, k != 0);
+            }
+            umma_commit(&s_full[hh]);
+          }
+          umma_commit(&k_empty[kst]);
+          if (j >= 1) umma_commit(&v_empty[(t - 1) % kPairVSt]);
+          if (j == n_kv - 1) umma_commit(q_empty);
+        }
+        mbar_wait(&v_full[(t - 1) % kPairVSt], ((t - 1) / kPairVSt) & 1);
+        tc_fence_after();
+        for (int hh = 0; hh < 2; ++hh) {
+          pv(hh, t - 1, n_kv == 1);
+          umma_commit(&o_done[hh]);
+        }
+        umma_commit(&v_empty[(t - 1) % kPairVSt]);
+        ++ic;
+      }
+    }
+  } else {
+    // ---------------- softmax: warpgroup hh = head, thread = query row ----------------
+    const int hh = (warp - 2) >> 2;
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t s_acc = t_s(hh) + lane_off, o_acc = t_o(hh) + lane_off;
+    uint32_t t = 0, ic = 0;
+    PairIter it(blockIdx.x, gridDim.x, n_items, n_qt_max, pairs, nseq, cu);
+    while (it.next()) {
+      const int n_kv = it.qt + 1;
+      const int qrow = it.qt * kT + r;
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < n_kv; ++j, ++t) {
+        // S(t) ready; pipe order also means every earlier P.V of this head is done (O stable)
+        mbar_wait(&s_full[hh], t & 1);
+        tc_fence_after();
+        float sv[kT];
+#pragma unroll
+        for (int c = 0; c < kT / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(s_acc + c * 32, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(v[i]) * scale_log2;
+        }
+        const int k0 = j * kT;
+        if (j == it.qt || k0 + kT > it.len) {
+#pragma unroll
+          for (int i = 0; i < kT; ++i)
+            if (k0 + i > qrow || k0 + i >= it.len) sv[i] = -INFINITY;
+        }
+        float mx = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < kT; ++i) mx = fmaxf(mx, sv[i]);
+        float corr = 1.f;
+        const bool rescale = mx > m_used + kRescaleThreshold;
+        if (rescale) {
+          corr = (m_used == -INFINITY) ? 0.f : fast_exp2(m_used - mx);
+          m_used = mx;
+        }
+        if (j >= 1 && __any_sync(0xffffffffu, rescale)) {
+#pragma unroll 1
+          for (int c = 0; c < kD / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld32(o_acc + c * 32, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
+            tmem_st32(o_acc + c * 32, v);
+          }
+        }
+        float sum = 0.f;
+        // P over the first 64 columns of this head's S accumulator, 32 keys at a time
+#pragma unroll
+        for (int c = 0; c < kT / 32; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float a = fast_exp2(sv[c * 32 + 2 * i] - m_used);
+            const float xb = sv[c * 32 + 2 * i + 1] - m_used;
+            const float b = (i & kPolyMask) ? exp2_poly(xb) : fast_exp2(xb);
+            sum += a + b;
+            pk[i] = pack_bf16x2(a, b);
+          }
+          tmem_st16(s_acc + c * 16, pk);
+        }
+        tmem_st_wait();
+        l = l * corr + sum;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[hh]);
+      }
+      // epilogue: O / l of this head, then hand O back to the MMA warp
+      mbar_wait(&o_done[hh], ic & 1);
+      tc_fence_after();
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      __nv_bfloat16* orow = out + static_cast<size_t>(it.start + qrow) * ldo + (2 * it.pair + hh) * kD;
+#pragma unroll 1
+      for (int c = 0; c < kD / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(o_acc + c * 32, v);
+        tmem_ld_wait();
+        if (qrow < it.len) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 o;
+            o.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]) * inv, __uint_as_float(v[8 * q + 1]) * inv);
+            o.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv);
+            o.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv);
+            o.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv);
+            dst[q] = o;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_free[hh]);
+      ++ic;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 }  // namespace
 
 int launch_prefill_attn_tc(const void* qkv, int ld, int T, int nq, int nk, const int32_t* cu, int nseq,
@@ -667,6 +1014,24 @@ int launch_prefill_attn_tc(const void* qkv, int ld, int T, int nq, int nk, const
   int rc = encode_tmap_2d_bf16(&map, qkv, static_cast<uint64_t>(ld), static_cast<uint64_t>(T),
                                static_cast<uint64_t>(ld) * 2, 64, kT);
   if (rc) return rc;
+  static const int force_single = [] {
+    const char* e = getenv("SSB_PREFILL_ATTN_SINGLE");  // A/B: 1 = one query head per CTA
+    return e ? atoi(e) : 0;
+  }();
+  if (persistent && (nq / nk) % 2 == 0 && !force_single) {
+    static bool pair_attr = false;
+    if (!pair_attr) {
+      SSB_CUDA(cudaFuncSetAttribute(prefill_attn_tc_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    SmemPair::kBytes));
+      pair_attr = true;
+    }
+    const int n_qt = (max_len + kT - 1) / kT;
+    const long items = static_cast<long>(n_qt) * (nq / 2) * nseq;
+    const int grid = static_cast<int>(std::min<long>(num_sms(), items));
+    prefill_attn_tc_pair<<<grid, kThreadsPair, SmemPair::kBytes, s>>>(
+        map, cu, nseq, n_qt, nq, nk, static_cast<__nv_bfloat16*>(out), ldo, scale * 1.4426950408889634f);
+    return check_launch("prefill_attn_tc_pair");
+  }
   if (persistent) {
     static bool pattr = false;
     if (!pattr) {

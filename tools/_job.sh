@@ -1,1 +1,3 @@
-SSB_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --prompts 16 --output-len 8 --steps 1 --warmup 3 --no-cpu-baseline 2>&1 | grep -v Warning | tail -3 | cut -c1-2500
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+SSB_PREFILL_ATTN_SINGLE=1 timeout 600 python tools/ab_bench.py --configs base --tag attn_single_head
+timeout 600 python tools/ab_bench.py --configs base --tag attn_pair_heads
