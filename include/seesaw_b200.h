@@ -68,6 +68,9 @@ int ssb_gemm_bf16(const void* A, const void* B, void* C, const void* R, int M, i
 /* block_n bits 20-27: force split-K into n k-ranges (needs a workspace). */
 #define SSB_GEMM_SPLIT_SHIFT 20
 #define SSB_GEMM_SPLIT(n) ((n) << SSB_GEMM_SPLIT_SHIFT)
+/* With SSB_GEMM_SPLIT(n): split only the tiles of the last, partial wave of
+ * the persistent schedule ("tail split"); full waves run whole tiles. */
+#define SSB_GEMM_TAIL (1 << 28)
 
 /* The same GEMM with a split-K workspace.  With block_n = 0 the library picks
  * (CTA pairs or single CTAs, N tile, number of k-splits) from a cost model of
@@ -85,7 +88,7 @@ int ssb_gemm_bf16_ws(const void* A, const void* B, void* C, const void* R, int M
                      int lda, int ldb, int ldc, int ldr, int epilogue, int block_n, int max_ctas,
                      void* workspace, int64_t workspace_bytes, void* stream);
 /* The configuration block_n = 0 would pick: out_plan[3] = {mode (0 single
- * CTA, 2 CTA pair), N tile, splits}; returns the workspace bytes it needs
+ * CTA, 2 CTA pair), N tile, splits (negative: tail split)}; returns the workspace bytes it needs
  * (0 without split-K), <0 on argument error. */
 int64_t ssb_gemm_plan(int M, int N, int K, int epilogue, int max_ctas, int64_t workspace_bytes,
                       int32_t* out_plan);

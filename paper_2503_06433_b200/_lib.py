@@ -21,6 +21,7 @@ SSB_GEMM_MC1 = 1 << 16
 SSB_GEMM_MC2 = 1 << 17
 SSB_GEMM_2SM = 1 << 18
 SSB_GEMM_SPLIT_SHIFT = 20
+SSB_GEMM_TAIL = 1 << 28
 SSB_MAX_PEERS = 64
 
 

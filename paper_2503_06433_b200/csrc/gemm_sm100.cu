@@ -83,6 +83,8 @@ struct Params {
   // k-block ranges of kb_per_split; the last warp to finish a tile quadrant
   // (counter) reduces the fp32 partials in split order and runs the epilogue
   int splits, kb_per_split;
+  int full_units;  // units [0, full_units) are whole tiles; the rest split `splits` ways
+                   // (0: every tile split; all units: no split) -- "tail split" fills the last wave
   float* ws;       // [tiles_m * tiles_n][splits][128][BN] fp32 partials
   int* counters;   // [tiles_m * tiles_n][4], zero between launches (self-resetting)
   RopeKV rk;       // SSB_EPI_ROPE_KV only
@@ -107,6 +109,20 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   const int o = local / gsize;
   tm = group_n ? o : b;
   tn = group_n ? b : o;
+}
+
+// Unit u of the persistent schedule -> (unit tile, split index, split count).
+__device__ __forceinline__ void unit_decode(const Params& p, int u, int& t, int& split, int& nsplit) {
+  if (u < p.full_units) {
+    t = u;
+    split = 0;
+    nsplit = 1;
+  } else {
+    const int v = u - p.full_units;
+    t = p.full_units + v / p.splits;
+    split = v - (v / p.splits) * p.splits;
+    nsplit = p.splits;
+  }
 }
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
@@ -333,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int num_units = units_m * p.tiles_n * p.splits;
+  const int num_units = p.full_units + (units_m * p.tiles_n - p.full_units) * p.splits;
   const int num_kb = (p.K + kBK - 1) / kBK;
 
   if (warp == 0 && lane == 0) {
@@ -390,10 +406,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int u = cid; u < num_units; u += nclusters) {
         int um, tn;
-        tile_coords(u / p.splits, units_m, p.tiles_n, p.group_n, p.group_size, um, tn);
+        int t, split, nsplit;
+        unit_decode(p, u, t, split, nsplit);
+        tile_coords(t, units_m, p.tiles_n, p.group_n, p.group_size, um, tn);
         const int tm = um * MC + crank;
-        const int kb0 = (u % p.splits) * p.kb_per_split;
-        const int kb1 = min(num_kb, kb0 + p.kb_per_split);
+        const int kb0 = nsplit > 1 ? split * p.kb_per_split : 0;
+        const int kb1 = nsplit > 1 ? min(num_kb, kb0 + p.kb_per_split) : num_kb;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (MODE == 2) {
@@ -439,8 +457,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        const int kb0 = (u % p.splits) * p.kb_per_split;
-        const int kb1 = min(num_kb, kb0 + p.kb_per_split);
+        int t, split, nsplit;
+        unit_decode(p, u, t, split, nsplit);
+        const int kb0 = nsplit > 1 ? split * p.kb_per_split : 0;
+        const int kb1 = nsplit > 1 ? min(num_kb, kb0 + p.kb_per_split) : num_kb;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -481,8 +501,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = cid; u < num_units; u += nclusters) {
-      int um, tn;
-      const int t = u / p.splits;
+      int um, tn, t, split, nsplit;
+      unit_decode(p, u, t, split, nsplit);
       tile_coords(t, units_m, p.tiles_n, p.group_n, p.group_size, um, tn);
       const int tm = um * MC + crank;
       mbar_wait(&tfull[acc], acc_phase);
@@ -490,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = tm * kBM + q * 32 + lane;
       const bool row_ok = row < p.M;
       const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      if (p.splits == 1) {
+      if (nsplit == 1) {
         if (p.epi == SSB_EPI_ARGMAX) {
           unsigned long long best = 0;
 #pragma unroll 1
@@ -562,10 +582,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // split-K: spill this split's fp32 partial, release TMEM, and let the
         // last of the tile quadrant's `splits` warps reduce + run the epilogue
         const int tile = tm * p.tiles_n + tn;
-        const int split = u % p.splits;
+        // partial slots are compact over the split unit tiles (x2 CTAs of a pair)
+        const size_t slot0 = static_cast<size_t>((t - p.full_units) * MC + crank) * nsplit;
         const size_t split_stride4 = static_cast<size_t>(kBM) * BN / 4;  // float4 per (tile, split)
-        float4* wbase = reinterpret_cast<float4*>(p.ws) +
-                        (static_cast<size_t>(tile) * p.splits + split) * split_stride4 + q * 32 + lane;
+        float4* wbase = reinterpret_cast<float4*>(p.ws) + (slot0 + split) * split_stride4 + q * 32 + lane;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           uint32_t a[32];
@@ -590,17 +610,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         int prev = 0;
         if (lane == 0) prev = atomicAdd(&p.counters[tile * 4 + q], 1);
         prev = __shfl_sync(0xffffffffu, prev, 0);
-        if (prev == p.splits - 1) {
+        if (prev == nsplit - 1) {
           __threadfence();
           if (lane == 0) p.counters[tile * 4 + q] = 0;  // every split arrived: reset for the next launch
-          const float4* rbase = reinterpret_cast<const float4*>(p.ws) +
-                                static_cast<size_t>(tile) * p.splits * split_stride4 + q * 32 + lane;
+          const float4* rbase = reinterpret_cast<const float4*>(p.ws) + slot0 * split_stride4 + q * 32 + lane;
           if (p.epi == SSB_EPI_ARGMAX) {
             unsigned long long best = 0;
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
               float f[32];
-              sum_partials(rbase, split_stride4, p.splits, c * 8, f);
+              sum_partials(rbase, split_stride4, nsplit, c * 8, f);
               argmax_cols(p, tn * BN + c * 32, f, best);
             }
             if (row_ok && best) atomicMax(reinterpret_cast<unsigned long long*>(p.C) + row, best);
@@ -609,23 +628,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int c = 0; c < BN / 32; ++c) {
               if (c & 2) continue;
               float fl[32], fh[32];
-              sum_partials(rbase, split_stride4, p.splits, c * 8, fl);
-              sum_partials(rbase, split_stride4, p.splits, (c + 2) * 8, fh);
+              sum_partials(rbase, split_stride4, nsplit, c * 8, fl);
+              sum_partials(rbase, split_stride4, nsplit, (c + 2) * 8, fh);
               if (row_ok && tn * BN + c * 32 < p.N) store_rope(p, row, tn * BN + c * 32, fl, fh);
             }
           } else if (p.epi == SSB_EPI_SILU_MUL) {
 #pragma unroll 1
             for (int c = 0; c < BN / 64; ++c) {
               float g[32], v[32];
-              sum_partials(rbase, split_stride4, p.splits, c * 16, g);
-              sum_partials(rbase, split_stride4, p.splits, c * 16 + 8, v);
+              sum_partials(rbase, split_stride4, nsplit, c * 16, g);
+              sum_partials(rbase, split_stride4, nsplit, c * 16 + 8, v);
               if (row_ok) store_silu(p, row, (tn * BN) / 2 + c * 32, g, v);
             }
           } else {
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
               float f[32];
-              sum_partials(rbase, split_stride4, p.splits, c * 8, f);
+              sum_partials(rbase, split_stride4, nsplit, c * 8, f);
               if (row_ok) store_cols(p, row, tn * BN + c * 32, f);
             }
           }
@@ -662,7 +681,7 @@ int gemm_policy_mode() {
 template <int BN, int MODE>
 int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, int K, int lda,
            int ldb, int ldc, int ldr, int epi, cudaStream_t stream, int max_ctas, int splits, void* ws,
-           const RopeKV* rk, int arg_base) {
+           const RopeKV* rk, int arg_base, bool tail) {
   using C = Cfg<BN, MODE>;
   constexpr int MC = MODE ? 2 : 1;
   CUtensorMap ta, tb;
@@ -710,10 +729,18 @@ int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, 
     p.group_n = n_band < m_band ? 1 : 0;
     if (band_env >= 0) p.group_n = band_env;
   }
-  const long units = static_cast<long>((p.tiles_m + MC - 1) / MC) * p.tiles_n * p.splits;
+  const long unit_tiles = static_cast<long>((p.tiles_m + MC - 1) / MC) * p.tiles_n;
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
-  grid = static_cast<int>(std::min<long>(grid / MC, units)) * MC;
+  const long groups = std::max(grid / MC, 1);
+  // tail split: whole tiles fill the full waves, only the last partial wave's
+  // tiles are split (so every group gets work in it); else every tile splits
+  if (p.splits <= 1)
+    p.full_units = static_cast<int>(unit_tiles);
+  else
+    p.full_units = tail ? static_cast<int>((unit_tiles / groups) * groups) : 0;
+  const long units = p.full_units + (unit_tiles - p.full_units) * p.splits;
+  grid = static_cast<int>(std::min<long>(groups, units)) * MC;
   if (MC == 1) {
     gemm_bf16_sm100<BN, MODE><<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, p);
   } else {
@@ -736,6 +763,7 @@ int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, 
 
 struct Plan {
   int mode, bn, splits;
+  int tail;  // split only the tiles of the last partial wave
 };
 
 // Tiles (128-row, including a pair's phantom tile when tiles_m is odd).
@@ -746,11 +774,17 @@ size_t plan_tiles(int M, int N, const Plan& pl) {
 
 // Workspace bytes of a split plan; SIZE_MAX when the tile counters do not fit
 // the fixed counter area.
-size_t plan_ws_bytes(int M, int N, const Plan& pl) {
+size_t plan_ws_bytes(int M, int N, const Plan& pl, int sms) {
   if (pl.splits <= 1) return 0;
+  const int MC = pl.mode ? 2 : 1;
   const size_t tiles = plan_tiles(M, N, pl);
   if (tiles * 4 * sizeof(int) > kCounterBytes) return SIZE_MAX;
-  return kCounterBytes + tiles * pl.splits * kBM * pl.bn * sizeof(float);
+  size_t split_tiles = tiles;
+  if (pl.tail) {
+    const size_t unit_tiles = tiles / MC, groups = std::max(sms / MC, 1);
+    split_tiles = (unit_tiles % groups) * MC;
+  }
+  return kCounterBytes + split_tiles * pl.splits * kBM * pl.bn * sizeof(float);
 }
 
 // Modelled time (microseconds) of one configuration: a fixed launch /
@@ -769,6 +803,17 @@ double plan_cost(int M, int N, int K, int sms, const Plan& pl) {
   const int kb = (K + kBK - 1) / kBK;
   const int kbs = (kb + pl.splits - 1) / pl.splits;
   const int splits = (kb + kbs - 1) / kbs;
+  if (pl.tail) {
+    // full waves of whole tiles, then ONE round of the split tail tiles
+    const long unit_tiles = static_cast<long>((tm + MC - 1) / MC) * ((N + pl.bn - 1) / pl.bn);
+    const long groups = std::max(1, sms / MC);
+    const long full = unit_tiles / groups, rem = unit_tiles % groups;
+    if (rem == 0 || rem * splits > groups) return 1e30;
+    double kb_us = pl.mode == 2 ? (pl.bn >= 256 ? 0.3839 : pl.bn >= 224 ? 0.3282 : pl.bn >= 192 ? 0.425 : 0.2417)
+                                : (pl.bn >= 256 ? 2.4031 : pl.bn >= 224 ? 1.435 : pl.bn >= 192 ? 0.3997 : 0.2308);
+    const double bytes = static_cast<double>(rem) * MC * splits * kBM * pl.bn * 4.0;
+    return 10.86 + full * kb * kb_us + kbs * kb_us + 8.19 + 0.03 * bytes / 1e6;
+  }
   const long units = static_cast<long>((tm + MC - 1) / MC) * ((N + pl.bn - 1) / pl.bn) * splits;
   const long groups = std::max(1, sms / MC);
   const long full = units / groups, rem = units % groups;
@@ -834,21 +879,26 @@ Plan choose_plan(int M, int N, int K, int epi, int sms, size_t ws_bytes) {
   static const int no_table = gemm_env("SSB_GEMM_NO_TABLE", 0);
   if (sms == num_sms() && !no_split && !no_table) {
     const Plan* m = measured_plan(M, N, K, epi);
-    if (m && (m->splits <= 1 || plan_ws_bytes(M, N, *m) <= ws_bytes)) return *m;
+    if (m && (m->splits <= 1 || plan_ws_bytes(M, N, *m, sms) <= ws_bytes)) return *m;
   }
   for (int mode = 0; mode <= 2; mode += 2) {
     if (mode == 2 && M <= kBM) continue;
     for (int bn : bns) {
       if (epi == SSB_EPI_SILU_MUL && bn % 64) continue;  // gate/up pairs of 32 columns
       if (epi == SSB_EPI_ROPE_KV && bn % 128) continue;  // whole heads per tile
-      for (int sp = 1; sp <= 16; ++sp) {
-        if (sp > 1 && (kb / sp < 4 || no_split)) break;
-        Plan pl{mode, bn, sp};
-        if (sp > 1 && plan_ws_bytes(M, N, pl) > ws_bytes) break;
-        const double t = plan_cost(M, N, K, sms, pl);
-        if (t < best_t * 0.995) {
-          best_t = t;
-          best = pl;
+      // tail splits are never chosen automatically: measured on the decode
+      // shapes (profiles/r01/gemm_plan_sweep_tail.jsonl) the partial-wave
+      // reduction costs what the filled last wave saves (W13: 99.3 vs 99.2 us)
+      for (int tail = 0; tail <= 0; ++tail) {
+        for (int sp = tail ? 2 : 1; sp <= 16; ++sp) {
+          if (sp > 1 && (kb / sp < 4 || no_split)) break;
+          Plan pl{mode, bn, sp, tail};
+          if (sp > 1 && plan_ws_bytes(M, N, pl, sms) > ws_bytes) break;
+          const double t = plan_cost(M, N, K, sms, pl);
+          if (t < best_t * 0.995) {
+            best_t = t;
+            best = pl;
+          }
         }
       }
     }
@@ -885,14 +935,16 @@ int gemm_entry(const void* A, const void* B, void* C, const void* R, int M, int 
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int sms = max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms();
-  Plan pl{0, block_n & 0xFFFF, 1};
+  Plan pl{0, block_n & 0xFFFF, 1, 0};
   const int forced_split = (block_n >> SSB_GEMM_SPLIT_SHIFT) & 0xFF;
+  const int forced_tail = (block_n & SSB_GEMM_TAIL) ? 1 : 0;
   if (pl.bn == 0 && !(block_n & (SSB_GEMM_MC1 | SSB_GEMM_MC2 | SSB_GEMM_2SM)) && forced_split == 0) {
     pl = choose_plan(M, N, K, epilogue, sms, static_cast<size_t>(ws_bytes));
   } else {
     pl.mode = (block_n & SSB_GEMM_2SM) ? 2 : (block_n & SSB_GEMM_MC2) ? 1 : 0;
     if (pl.bn == 0) pl.bn = 256;
     pl.splits = forced_split ? forced_split : 1;
+    pl.tail = forced_tail;
     if (pl.mode == 2 && M <= kBM) pl.mode = 0;
   }
   if (epilogue == SSB_EPI_SILU_MUL && pl.bn % 64)
@@ -903,17 +955,17 @@ int gemm_entry(const void* A, const void* B, void* C, const void* R, int M, int 
     const int kb = (K + kBK - 1) / kBK, kbs = (kb + pl.splits - 1) / pl.splits;
     pl.splits = (kb + kbs - 1) / kbs;
   }
-  if (pl.splits > 1 && plan_ws_bytes(M, N, pl) > static_cast<size_t>(ws_bytes))
+  if (pl.splits > 1 && plan_ws_bytes(M, N, pl, sms) > static_cast<size_t>(ws_bytes))
     return fail_arg("ssb_gemm_bf16: split-K x%d needs %zu workspace bytes, have %lld", pl.splits,
-                    plan_ws_bytes(M, N, pl), static_cast<long long>(ws_bytes));
+                    plan_ws_bytes(M, N, pl, sms), static_cast<long long>(ws_bytes));
 #define SSB_GEMM_CASE(BN_)                                                                              \
   case BN_:                                                                                            \
     return pl.mode == 2   ? launch<BN_, 2>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas, \
-                                           pl.splits, workspace, rk, arg_base)                         \
+                                           pl.splits, workspace, rk, arg_base, pl.tail != 0)           \
            : pl.mode == 1 ? launch<BN_, 1>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas, \
-                                           pl.splits, workspace, rk, arg_base)                         \
+                                           pl.splits, workspace, rk, arg_base, pl.tail != 0)           \
                           : launch<BN_, 0>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas, \
-                                           pl.splits, workspace, rk, arg_base);
+                                           pl.splits, workspace, rk, arg_base, pl.tail != 0);
   switch (pl.bn) {
     SSB_GEMM_CASE(256)
     SSB_GEMM_CASE(224)
@@ -947,9 +999,9 @@ extern "C" int64_t ssb_gemm_plan(int M, int N, int K, int epilogue, int max_ctas
   if (out_plan) {
     out_plan[0] = pl.mode;
     out_plan[1] = pl.bn;
-    out_plan[2] = pl.splits;
+    out_plan[2] = pl.tail ? -pl.splits : pl.splits;  // negative: tail split
   }
-  return static_cast<int64_t>(plan_ws_bytes(M, N, pl));
+  return static_cast<int64_t>(plan_ws_bytes(M, N, pl, sms));
 }
 
 extern "C" int ssb_gemm_qkv_rope_kv(const void* A, const void* B, void* qkv, int M, int K, int lda, int ldb,

@@ -185,3 +185,38 @@ def test_gemm_split_k_shared_workspace_sequence(cuda):
         ref = _ref(a, w)
         assert (out.float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item() + 1e-2, (M, N, K, bn, sp)
         assert int(ws[: 64 << 10].view(torch.int32).abs().sum()) == 0
+
+
+@pytest.mark.parametrize("mode", ["single", "2sm"])
+@pytest.mark.parametrize("M,N,K,bn,splits", [(512, 28672, 4096, 256, 4), (512, 40000, 1024, 128, 2),
+                                             (300, 20000, 2048, 192, 3), (512, 19200, 512, 256, 8)])
+def test_gemm_tail_split(cuda, mode, M, N, K, bn, splits):
+    """Tail split: whole tiles in the full waves, only the last partial wave's
+    tiles split K -- every epilogue, deterministic, counters left zero."""
+    from paper_2503_06433_b200._lib import SSB_GEMM_2SM, SSB_GEMM_SPLIT_SHIFT, SSB_GEMM_TAIL
+
+    flag = bn | (splits << SSB_GEMM_SPLIT_SHIFT) | SSB_GEMM_TAIL | (SSB_GEMM_2SM if mode == "2sm" else 0)
+    g = torch.Generator(device="cuda").manual_seed(N + splits)
+    a = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=cuda, generator=g) / K**0.5).to(torch.bfloat16)
+    ws = _ws(cuda, 160 << 20)
+    out = ops.gemm(a, w, block_n=flag, workspace=ws)
+    out2 = ops.gemm(a, w, block_n=flag, workspace=ws)
+    torch.cuda.synchronize()
+    ref = _ref(a, w)
+    assert (out.float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item() + 1e-2
+    assert torch.equal(out, out2)
+    assert int(ws[: 64 << 10].view(torch.int32).abs().sum()) == 0
+    r = torch.randn(M, N, device=cuda, generator=g).to(torch.bfloat16)
+    exp = ref + r.float()
+    ops.gemm(a, w, out=r, residual=r, block_n=flag, workspace=ws)
+    torch.cuda.synchronize()
+    assert (r.float() - exp).abs().max().item() <= 2e-2 * exp.abs().max().item() + 2e-2
+    if bn % 64 == 0 and N % 64 == 0:
+        F = N // 2
+        s = ops.gemm(a, w, silu_mul=True, block_n=flag, workspace=ws)
+        torch.cuda.synchronize()
+        wv = w.view(F // 32, 2, 32, K)
+        sref = torch.nn.functional.silu(a.float() @ wv[:, 0].reshape(F, K).float().T) * (
+            a.float() @ wv[:, 1].reshape(F, K).float().T)
+        assert (s.float() - sref).abs().max().item() < 3e-2 * sref.abs().max().item() + 1e-2

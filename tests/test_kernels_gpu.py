@@ -124,8 +124,11 @@ def test_qkv_gemm_rope_kv_fused_bit_exact(cuda, M, nq, nk, K, neg, flag):
     if flag == "auto":  # the unfused reference runs the plan the fused launch picks (same fp32 sums)
         from paper_2503_06433_b200._lib import SSB_EPI_ROPE_KV
 
+        from paper_2503_06433_b200._lib import SSB_GEMM_TAIL
+
         (mode, pbn, sp), _ = ops.gemm_plan(M, w.shape[0], K, SSB_EPI_ROPE_KV, 0, ws.numel())
-        ref_bn = pbn | (SSB_GEMM_2SM if mode == 2 else 0) | (sp << SSB_GEMM_SPLIT_SHIFT if sp > 1 else 0)
+        ref_bn = pbn | (SSB_GEMM_2SM if mode == 2 else 0) | (abs(sp) << SSB_GEMM_SPLIT_SHIFT if abs(sp) > 1 else 0)
+        ref_bn |= SSB_GEMM_TAIL if sp < 0 else 0
     else:
         ref_bn = bn
     ref = ops.gemm(a, w, workspace=ws, block_n=ref_bn)

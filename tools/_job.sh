@@ -1,3 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
-SSB_PREFILL_ATTN_SINGLE=1 timeout 600 python tools/ab_bench.py --configs base --tag attn_single_head
-timeout 600 python tools/ab_bench.py --configs base --tag attn_pair_heads
+timeout 600 python -m pytest tests/test_gemm_gpu.py tests/test_kernels_gpu.py -q -x 2>&1 | tail -3
+timeout 900 python tools/bench_kernels.py --what splitk > gpurun_out/kb_splitk4.log 2>&1; tail -2 gpurun_out/kb_splitk4.log | cut -c1-300

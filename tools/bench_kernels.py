@@ -88,7 +88,7 @@ if __name__ == "__main__":
 
 def bench_splitk():
     """Forced (mode, bn, splits) sweep vs the auto plan on decode shapes."""
-    from paper_2503_06433_b200._lib import SSB_GEMM_2SM, SSB_GEMM_SPLIT_SHIFT
+    from paper_2503_06433_b200._lib import SSB_GEMM_2SM, SSB_GEMM_SPLIT_SHIFT, SSB_GEMM_TAIL
 
     ws = torch.zeros(256 << 20, dtype=torch.uint8, device="cuda")
     shapes = [(M, N, K) for M in (512, 256) for N, K in
@@ -111,12 +111,14 @@ def bench_splitk():
                 for sp in ((1,) if M > 4096 else (1, 2, 3, 4, 6, 8)):
                     if K // 64 // sp < 2:
                         continue
-                    flag = bn | (sp << SSB_GEMM_SPLIT_SHIFT) | (SSB_GEMM_2SM if mode == 2 else 0)
-                    try:
-                        ms = timed(lambda: ops.gemm(a, w, out=c, block_n=flag, workspace=ws), iters=10)
-                    except Exception as e:  # noqa: BLE001
-                        continue
-                    res.append((f"m{mode}b{bn}s{sp}", None, ms))
+                    for tail in ((0, 1) if sp > 1 else (0,)):
+                        flag = bn | (sp << SSB_GEMM_SPLIT_SHIFT) | (SSB_GEMM_2SM if mode == 2 else 0)
+                        flag |= SSB_GEMM_TAIL if tail else 0
+                        try:
+                            ms = timed(lambda: ops.gemm(a, w, out=c, block_n=flag, workspace=ws), iters=10)
+                        except Exception as e:  # noqa: BLE001
+                            continue
+                        res.append((f"m{mode}b{bn}s{sp}" + ("t" if tail else ""), None, ms))
         best = min(res[2:], key=lambda r: r[2])
         print(json.dumps({"M": M, "N": N, "K": K, "auto_plan": res[0][1], "auto_ms": res[0][2],
                           "auto_tflops": fl / res[0][2] / 1e9, "cublas_ms": ms_t, "cublas_tflops": fl / ms_t / 1e9,
