@@ -465,6 +465,7 @@ __global__ void __launch_bounds__(128)
   const int G = nq / nk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_items = B * nk;
+  griddep_launch_dependents();
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmap);

@@ -778,6 +778,7 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
   const int group = nq / nk;
   const int n_items = n_qt_max * pairs * nseq;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  griddep_launch_dependents();
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmap);

@@ -378,6 +378,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (MC > 1) cluster_sync_all();  // peer barriers initialised before any multicast lands
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // PDL: everything above (barrier init, TMEM allocation, descriptor
+  // prefetch) overlapped the previous kernel; from here on global memory the
+  // previous kernel writes (A, the residual / output) is touched
+  griddep_launch_dependents();
+  if (warp != 1) griddep_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -741,21 +746,29 @@ int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, 
     p.full_units = tail ? static_cast<int>((unit_tiles / groups) * groups) : 0;
   const long units = p.full_units + (unit_tiles - p.full_units) * p.splits;
   grid = static_cast<int>(std::min<long>(groups, units)) * MC;
-  if (MC == 1) {
-    gemm_bf16_sm100<BN, MODE><<<grid, kThreads, C::kSmemBytes, stream>>>(ta, tb, p);
-  } else {
+  {
+    static const int pdl = gemm_env("SSB_PDL", 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = C::kSmemBytes;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = MC;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2];
+    int n = 0;
+    if (MC > 1) {
+      attr[n].id = cudaLaunchAttributeClusterDimension;
+      attr[n].val.clusterDim.x = MC;
+      attr[n].val.clusterDim.y = 1;
+      attr[n].val.clusterDim.z = 1;
+      ++n;
+    }
+    if (pdl) {
+      attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[n].val.programmaticStreamSerializationAllowed = 1;
+      ++n;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = n;
     SSB_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_sm100<BN, MODE>, ta, tb, p));
   }
   return check_launch("gemm_bf16_sm100");

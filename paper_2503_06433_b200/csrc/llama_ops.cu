@@ -19,6 +19,7 @@ __global__ void __launch_bounds__(kNormThreads)
     rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, int ldx, const int32_t* __restrict__ row_idx,
                    const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ out, int ldo, int hidden,
                    float eps) {
+  griddep_launch_dependents();  // the next (PDL-launched) GEMM may start its prologue
   const int row = blockIdx.x;
   const int src_row = row_idx ? row_idx[row] : row;
   const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<size_t>(src_row) * ldx);

@@ -1,2 +1,4 @@
-timeout 600 python -m pytest tests/test_gemm_gpu.py tests/test_kernels_gpu.py -q -x 2>&1 | tail -3
-timeout 900 python tools/bench_kernels.py --what splitk > gpurun_out/kb_splitk4.log 2>&1; tail -2 gpurun_out/kb_splitk4.log | cut -c1-300
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+SSB_PDL=0 timeout 600 python tools/ab_bench.py --configs base --tag pdl_off
+timeout 600 python tools/ab_bench.py --configs base --tag pdl_on
+SSB_PDL=0 timeout 600 python tools/ab_bench.py --configs base --tag pdl_off
