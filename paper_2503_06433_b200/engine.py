@@ -335,13 +335,27 @@ class _Engine:
         gpus = self.cfg_p.gpus_per_replica
         staging = self.max_prompt * self.kv_tok // gpus
         a = self.arch
-        key = ("tier", self.max_prompt, max(n_slots, 1), staging)
-        cache = w.__dict__.setdefault("_tier_cache", {})
-        if key not in cache:  # pinned memory is allocated once per worker and shape
-            cache[key] = HostTier(w.replica_comm, self.device, a.num_layers, a.num_kv_heads, a.head_dim,
-                                  self.max_prompt, max(n_slots, 1), staging)
-        self.tier = cache[key]
-        self.tier.free = list(range(self.tier.n_slots))
+        # pinned memory is allocated once per worker and reused by later runs
+        # whose slot shape matches and whose slot count it covers; a larger
+        # need replaces it (the old buffer is released first: pinned host
+        # memory, not HBM, is what runs out at 13B/70B scale)
+        shape = (self.max_prompt, staging)
+        tier = getattr(w, "_host_tier", None)
+        if tier is None or tier.shape_key != shape or tier.n_slots < max(n_slots, 1):
+            w._host_tier = None
+            del tier
+            import gc
+
+            gc.collect()
+            if self.device.type == "cuda":
+                torch.cuda.synchronize(self.device)
+                torch._C._host_emptyCache()  # return cached pinned blocks to the OS
+            tier = HostTier(w.replica_comm, self.device, a.num_layers, a.num_kv_heads, a.head_dim,
+                            self.max_prompt, max(n_slots, 1), staging)
+            tier.shape_key = shape
+            w._host_tier = tier
+        self.tier = tier
+        self.tier.free = list(range(max(n_slots, 1)))
         self.slots_total = max(n_slots, 1)
         # deterministic admission lag (decode steps) for a swap-in: transfer
         # time of one sequence's piece at the host link rate over a nominal

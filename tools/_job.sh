@@ -1,4 +1,1 @@
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
-SSB_PDL=0 timeout 600 python tools/ab_bench.py --configs base --tag pdl_off
-timeout 600 python tools/ab_bench.py --configs base --tag pdl_on
-SSB_PDL=0 timeout 600 python tools/ab_bench.py --configs base --tag pdl_off
+timeout 1500 python tools/bench_tier.py --arch llama2-13b --prompts 256 --kv-gb 110 --host-gb 110 > gpurun_out/tier13.log 2>&1; grep -v "Warning\|^\[W" gpurun_out/tier13.log | tail -30 | cut -c1-300

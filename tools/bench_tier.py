@@ -94,7 +94,8 @@ def main() -> None:
     host_bytes = swapped * args.input_len * kv_tok
     out = {
         "workload": f"{arch.name} {args.prompts} x {args.input_len}/{args.output_len}, PP1->TP1 on 1 B200, "
-                    f"GPU KV pool {args.kv_gb:.0f} GB + pinned host tier (BASELINE configs[3] shape)",
+                    f"GPU KV pool {args.kv_gb:.0f} GB + pinned host tier "
+                    f"(BASELINE {'configs[3]' if '70b' in arch.name else 'configs[2] model'} shape)",
         "tokens_per_s": rep.tokens_per_second,
         "makespan_s": rep.makespan,
         "device_timed_s": wall,
