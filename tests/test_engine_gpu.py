@@ -244,3 +244,81 @@ def test_host_tier_single_gpu(cuda):
     rep = res[0][0]
     assert rep.config["host_tier"] and replay_check(rep)
     check_greedy(arch, reqs, prompts, rep.outputs, 1, 1)
+
+
+def _run_ragged(arch_name, cfg_p, cfg_d, lens, gpu_seqs=None, gpu_memory=2e9, record_logits=False):
+    """Ragged workload (every request its own input and output length)."""
+    from paper_2503_06433_b200.specs import kv_bytes_per_token, total_weight_bytes
+
+    arch = PRESETS[arch_name]
+    model = arch.model_spec()
+    W = cfg_p.num_gpus
+    reqs = [Request(i, a, b) for i, (a, b) in enumerate(lens)]
+    hw = tiny_hw(W, gpu_memory=gpu_memory)
+    if gpu_seqs is not None:
+        k = max(a + b for a, b in lens) * kv_bytes_per_token(model)
+        hw = tiny_hw(W, gpu_memory=(total_weight_bytes(model) + gpu_seqs * k) / W,
+                     host_memory_per_gpu=len(lens) * k / W)
+    prompts = synthetic_prompts(reqs, arch.vocab)
+    comms = ThreadComm.create(W)
+
+    def body(r):
+        dev = torch.device("cuda", 0)
+        wk = Worker(arch, comms[r], cfg_p.dp, dev, seed=0, max_pos=512)
+        rep = execute(model, hw, reqs, SchedulingPolicy.TRANSITION_MINIMIZING, cfg_p, cfg_d, arch=arch,
+                      prompts=prompts, comm=comms[r], device=dev, worker=wk, record_logits=record_logits)
+        return (rep, [x.clone() for x in wk.logit_log]) if record_logits else rep
+
+    return arch, reqs, prompts, run_threads(W, body)
+
+
+RAGGED = [(17, 5), (130, 40), (64, 1), (1, 9), (200, 12), (65, 64), (3, 30), (127, 2), (90, 33), (45, 17)]
+
+
+@pytest.mark.parametrize("gpu_seqs", [None, 4])
+def test_ragged_lengths_pp2_to_tp2(cuda, gpu_seqs):
+    """Ragged prompts and output lengths (1-token prompts, 1-token outputs,
+    block-boundary lengths): varlen prefill, sequences released at different
+    decode steps (the batch shrinks and the GEMM plans change shape), with and
+    without the host tier; tokens match the oracle, the log replays."""
+    arch, reqs, prompts, res = _run_ragged("tiny", ParallelismConfig(1, 2, 1), ParallelismConfig(2, 1, 1), RAGGED,
+                                           gpu_seqs=gpu_seqs)
+    rep = res[0]
+    assert replay_check(rep), replay_check(rep).violation
+    assert rep.outputs == res[1].outputs
+    if gpu_seqs is not None:
+        assert rep.config["host_tier"]
+    check_greedy(arch, reqs, prompts, rep.outputs, 1, 2)
+
+
+def test_ragged_lengths_llama_shape_single_gpu(cuda):
+    """The same ragged workload through the Llama-3-8B kernels (head_dim 128:
+    fused RoPE/K-V append, tcgen05 pair attention, split-K GEMM plans) on a
+    2-layer model: PP1 -> TP1 (all prompts in one packed forward) against
+    PP2 -> TP2 (one prompt per micro-batch, re-shard, TP decode).  Prefill
+    logits agree within bf16 tolerance; first tokens may differ only at near
+    ties (random-init logits over a 128k vocabulary have many)."""
+    import dataclasses
+
+    base = PRESETS["llama3-8b"]
+    arch = dataclasses.replace(base, num_layers=2, name="llama3-8b-2l")
+    PRESETS["llama3-8b-2l"] = arch
+    try:
+        _, reqs, _, one = _run_ragged("llama3-8b-2l", ParallelismConfig(1, 1, 1), ParallelismConfig(1, 1, 1), RAGGED,
+                                      gpu_memory=40e9, record_logits=True)
+        _, _, _, two = _run_ragged("llama3-8b-2l", ParallelismConfig(1, 2, 1), ParallelismConfig(2, 1, 1), RAGGED,
+                                   gpu_memory=20e9, record_logits=True)
+    finally:
+        PRESETS.pop("llama3-8b-2l", None)
+    (rep1, logs1), (rep2, _), (_, logs2) = one[0], two[0], two[1]
+    assert replay_check(rep1) and replay_check(rep2) and rep2.transitions == 1
+    pre1 = logs1[0]                          # [10, V]: one packed forward
+    pre2 = torch.cat(logs2[: len(reqs)])     # one micro-batch per prompt on the last stage
+    scale = pre1.abs().max().item()
+    assert (pre1 - pre2).abs().max().item() < 0.05 * scale + 0.05
+    for i, r in enumerate(reqs):
+        a, b = rep1.outputs[r.id], rep2.outputs[r.id]
+        assert len(a) == len(b) == r.output_len
+        if a[0] != b[0]:
+            top = torch.topk(pre1[i], 2).values
+            assert float(top[0] - top[1]) < 0.05 * scale, (r.id, a[0], b[0])
