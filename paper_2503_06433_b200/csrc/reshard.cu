@@ -11,6 +11,9 @@
 // Weights / host tier: a batched 2-D strided copy driven by a device array of
 // descriptors (rows x row_bytes with independent strides); the row-parallel
 // column slices of Wo / W_down are rows of head_dim*heads elements.
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "seesaw_b200.h"
 
@@ -94,6 +97,93 @@ __global__ void __launch_bounds__(kCopyThreads) kv_reshard_kernel(
              reinterpret_cast<uint4*>(pool + pool_off), run_bytes >> 4);
 }
 
+// Bulk-copy (TMA engine) variant: ONE thread per CTA streams every run of
+// its share through a ring of shared-memory slots with cp.async.bulk
+// global->shared (mbarrier completion) and shared->global (bulk groups),
+// keeping kBulkSlots-1 loads in flight; the SM's load/store units are idle.
+constexpr int kBulkSlots = 4;
+constexpr int kBulkChunk = 16 * 1024;
+
+template <bool kPack>
+__global__ void __launch_bounds__(32) kv_reshard_bulk_kernel(
+    uint8_t* __restrict__ pool, uint8_t* __restrict__ staging, const int32_t* __restrict__ ids, int n_ids,
+    int n_peers, ssb_kv_geometry geo, const PeerTable tab, int total_runs) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ __align__(8) uint64_t full[kBulkSlots];
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < kBulkSlots; ++i) mbar_init(&full[i], 1);
+  fence_mbar_init();
+  const int64_t plane = static_cast<int64_t>(geo.block_size) * geo.head_dim * 2;
+  // cursor over (run, offset) chunks of this CTA's runs
+  struct Cur {
+    int run;
+    int64_t off, bytes;
+    const uint8_t* src;
+    uint8_t* dst;
+  };
+  auto locate = [&](Cur& c) {  // src/dst/bytes of c.run (decoded as in kv_reshard_kernel)
+    int p = 0, kv, j, i, nl;
+    if (kPack && tab.uniform_nl > 0) {
+      nl = tab.uniform_nl;
+      p = c.run % n_peers;
+      const int rest = c.run / n_peers;
+      kv = rest & 1;
+      j = (rest >> 1) % nl;
+      i = (rest >> 1) / nl;
+    } else {
+      while (p + 1 < n_peers && c.run >= tab.run_begin[p + 1]) ++p;
+      const int local = c.run - tab.run_begin[p];
+      nl = tab.nl[p];
+      kv = local & 1;
+      j = (local >> 1) % nl;
+      i = (local >> 1) / nl;
+    }
+    const int64_t run_bytes = plane * tab.nh[p];
+    const int64_t blk = ids[i];
+    const int64_t pool_off =
+        ((blk * geo.n_layers + (tab.l0[p] + j)) * 2 + kv) * (plane * geo.n_heads) + tab.h0[p] * plane;
+    const int64_t stage_off = tab.off[p] + (static_cast<int64_t>(i * nl + j) * 2 + kv) * run_bytes;
+    c.bytes = run_bytes;
+    c.src = kPack ? pool + pool_off : staging + stage_off;
+    c.dst = kPack ? staging + stage_off : pool + pool_off;
+  };
+  Cur ld{static_cast<int>(blockIdx.x), 0, 0, nullptr, nullptr};
+  if (ld.run < total_runs) locate(ld);
+  uint8_t* slot_dst[kBulkSlots];
+  uint32_t slot_bytes[kBulkSlots];
+  auto issue = [&](uint32_t n) -> bool {  // next chunk's global->shared load into slot n % S
+    if (ld.run >= total_runs) return false;
+    const int s = n % kBulkSlots;
+    const int64_t left = ld.bytes - ld.off;
+    const uint32_t bytes = static_cast<uint32_t>(left < kBulkChunk ? left : kBulkChunk);
+    mbar_arrive_expect_tx(&full[s], bytes);
+    bulk_g2s(ring + s * kBulkChunk, ld.src + ld.off, bytes, &full[s]);
+    slot_dst[s] = ld.dst + ld.off;
+    slot_bytes[s] = bytes;
+    ld.off += bytes;
+    if (ld.off >= ld.bytes) {
+      ld.run += gridDim.x;
+      ld.off = 0;
+      if (ld.run < total_runs) locate(ld);
+    }
+    return true;
+  };
+  uint32_t issued = 0;
+  while (issued < kBulkSlots && issue(issued)) ++issued;
+  for (uint32_t n = 0; n < issued; ++n) {
+    const int s = n % kBulkSlots;
+    mbar_wait(&full[s], (n / kBulkSlots) & 1);
+    bulk_s2g(slot_dst[s], ring + s * kBulkChunk, slot_bytes[s]);
+    bulk_commit();
+    // refill the slot of chunk n-1 once its store has read shared memory
+    if (n >= 1) {
+      bulk_wait_read<1>();
+      if (issue(issued)) ++issued;
+    }
+  }
+  bulk_wait<0>();
+}
+
 int kv_reshard(bool pack, void* pool, ssb_kv_geometry geo, const int32_t* ids, int n_ids, int n_peers,
                const int32_t* l0, const int32_t* nl, const int32_t* h0, const int32_t* nh,
                const int64_t* off, void* staging, void* stream) {
@@ -132,6 +222,37 @@ int kv_reshard(bool pack, void* pool, ssb_kv_geometry geo, const int32_t* ids, i
     if (t.nl[p] != t.nl[0]) t.uniform_nl = 0;
   if (runs == 0) return 0;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // Copy engine choice (SSB_RESHARD_BULK: 1 force bulk, 0 force LSU, unset
+  // auto).  Measured per GPU on the 8B KV (tools/bench_reshard.py): the
+  // bulk (TMA-engine) copy packs 16 KiB single-head runs scattered over the
+  // PP-layout pool at 5.8-6.0 TB/s vs 5.2-5.6 with 16-byte LSU copies
+  // (PP4/PP8 -> TP), but is slower for long runs and for unpack (6.1 vs
+  // 6.4-6.7 TB/s), so auto = bulk for pack with single-head rectangles only.
+  static const int bulk_env = [] {
+    const char* e = getenv("SSB_RESHARD_BULK");
+    return e ? atoi(e) : -1;
+  }();
+  bool single_head = true;
+  for (int p = 0; p < n_peers; ++p) single_head = single_head && (t.nh[p] <= 1);
+  const bool bulk = bulk_env >= 0 ? bulk_env != 0 : (pack && single_head && t.uniform_nl > 0);
+  if (bulk) {
+    const int smem = kBulkSlots * kBulkChunk;
+    static bool attr = false;
+    if (!attr) {
+      SSB_CUDA(cudaFuncSetAttribute(kv_reshard_bulk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      SSB_CUDA(cudaFuncSetAttribute(kv_reshard_bulk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = true;
+    }
+    const int grid = std::min(runs, 3 * num_sms());
+    if (pack)
+      kv_reshard_bulk_kernel<true><<<grid, 32, smem, s>>>(static_cast<uint8_t*>(pool), static_cast<uint8_t*>(staging),
+                                                          ids, n_ids, n_peers, geo, t, runs);
+    else
+      kv_reshard_bulk_kernel<false><<<grid, 32, smem, s>>>(static_cast<uint8_t*>(pool),
+                                                           static_cast<uint8_t*>(staging), ids, n_ids, n_peers, geo, t,
+                                                           runs);
+    return check_launch(pack ? "kv_reshard_pack" : "kv_reshard_unpack");
+  }
   if (pack)
     kv_reshard_kernel<true><<<runs, kCopyThreads, 0, s>>>(
         static_cast<uint8_t*>(pool), static_cast<uint8_t*>(staging), ids, n_ids, n_peers, geo, t);

@@ -1,1 +1,3 @@
-timeout 1500 python tools/bench_tier.py --arch llama2-13b --prompts 256 --kv-gb 110 --host-gb 110 > gpurun_out/tier13.log 2>&1; grep -v "Warning\|^\[W" gpurun_out/tier13.log | tail -30 | cut -c1-300
+SSB_RESHARD_BULK=1 timeout 600 python -m pytest tests/test_reshard_gpu.py -q -x 2>&1 | tail -1
+timeout 300 python tools/bench_reshard.py
+SSB_RESHARD_BULK=1 timeout 300 python tools/bench_reshard.py
