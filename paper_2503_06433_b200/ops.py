@@ -8,6 +8,7 @@ only; every op here runs one of the library's sm_100a kernels.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import torch
 
@@ -25,7 +26,8 @@ def gemm_plan(M: int, N: int, K: int, epilogue: int = SSB_EPI_NONE, max_ctas: in
     return (out[0], out[1], out[2]), int(need)
 
 
-_PREFILL_VARIANT = int(__import__("os").environ.get("SSB_PREFILL_ATTN_VARIANT", "0"))
+# prefill attention kernel variant for A/B runs (see ssb_prefill_attention)
+_PREFILL_VARIANT = int(os.environ.get("SSB_PREFILL_ATTN_VARIANT", "0"))
 
 
 def _stream() -> int:
