@@ -507,8 +507,20 @@ __global__ void __launch_bounds__(128)
     ++p_count;
     ++p_blk;
   };
+  // PDL: this kernel may start while the QKV GEMM that appends the current
+  // token's K/V (and writes Q) still runs.  Every pool block but a sequence's
+  // LAST one holds only older tokens, so those may stream into the ring now;
+  // Q and the last blocks are read only after griddep_wait().
+  int issued = 0;
+  if (threadIdx.x == 0) {
+    while (issued < kPStages && p_seek() && p_blk + 1 < p_nblk) {
+      issue_next();
+      ++issued;
+    }
+  }
+  griddep_wait();
   if (threadIdx.x == 0)
-    for (int i = 0; i < kPStages; ++i) issue_next();
+    for (; issued < kPStages; ++issued) issue_next();
 
   uint32_t c_count = 0;  // blocks consumed so far
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
@@ -680,9 +692,23 @@ int launch_decode_p(const CUtensorMap& map, const void* qkv, int ld, int nq, int
   if (ctas_per_sm > 0) per_sm = std::min(per_sm, ctas_per_sm);
   const long items = static_cast<long>(B) * nk;
   const int grid = static_cast<int>(std::min<long>(items, static_cast<long>(std::max(per_sm, 1)) * num_sms()));
-  decode_attn_persistent<D, ST><<<grid, 128, smem, s>>>(map, static_cast<const __nv_bfloat16*>(qkv), ld, nq, nk, tables,
-                                                       max_blocks, ctx, B, geo, layer, static_cast<__nv_bfloat16*>(out),
-                                                       ldo, scale * kLog2e);
+  static const int pdl = [] {
+    const char* e = getenv("SSB_PDL");
+    return e ? atoi(e) : 1;
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  SSB_CUDA(cudaLaunchKernelEx(&cfg, decode_attn_persistent<D, ST>, map, static_cast<const __nv_bfloat16*>(qkv), ld, nq,
+                              nk, tables, max_blocks, ctx, B, geo, layer, static_cast<__nv_bfloat16*>(out), ldo,
+                              scale * kLog2e));
   return check_launch("decode_attn_persistent");
 }
 
