@@ -46,13 +46,16 @@ def main() -> None:
         w.fuse_argmax = name != "no_argmax_fusion"
         w.split_k = name != "no_split_k"
         ops._PREFILL_VARIANT = 2 if name == "attn_per_tile_ctas" else 0
+        state["prefill_tokens"] = {"prefill_8k": 8192, "prefill_32k": 32768}.get(name, 16384)
+
+    state = {"prefill_tokens": 16384}
 
     def batch():
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         rep = execute(model, hw, reqs, SchedulingPolicy.TRANSITION_MINIMIZING, cfg, cfg, arch=arch, prompts=prompts,
-                      comm=SoloComm(), device=dev, worker=w)
+                      comm=SoloComm(), device=dev, worker=w, max_prefill_tokens=state["prefill_tokens"])
         e.record()
         torch.cuda.synchronize()
         return s.elapsed_time(e) / 1e3, rep
