@@ -65,3 +65,27 @@ def test_trace_with_prompts(tmp_path):
                  '{"input_len": 2, "output_len": 1, "prompt": [5, 6]}\n')
     reqs, prompts = parse_trace(t)
     assert [r.id for r in reqs] == ["a", 1] and prompts == [[1, 2, 3], [5, 6]]
+
+
+def test_calibration_reproduces_measured_phases(tmp_path):
+    """tools/calibrate.py fits the reference model's HardwareSpec to the
+    committed bench line; the fitted spec loads with the reference loader and
+    reproduces the measured phase times."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    line = root / "profiles" / "r01" / "bench_line_final.jsonl"
+    out = tmp_path / "hw.yaml"
+    p = subprocess.run([sys.executable, str(root / "tools" / "calibrate.py"), str(line), str(out)],
+                       capture_output=True, text=True, timeout=120)
+    assert p.returncode == 0, p.stderr
+    res = json.loads(p.stdout)
+    m, c = res["measured"], res["reference_model_calibrated"]
+    assert abs(c["prefill_s"] / m["prefill_s"] - 1) < 0.01 and abs(c["decode_s"] / m["decode_s"] - 1) < 0.01
+    from paper_2503_06433_b200.specs import load_hardware_spec
+
+    hw = load_hardware_spec(out)
+    assert hw.peak_flops == float(f"{c['hw']['peak_flops']:.4e}")
