@@ -288,8 +288,10 @@ def argmax_combine(vals: torch.Tensor, idxs: torch.Tensor, out_idx: torch.Tensor
 
 def prefill_attention(qkv: torch.Tensor, nq: int, nk: int, head_dim: int, cu_seqlens: torch.Tensor,
                       max_len: int, out: torch.Tensor, scale: float, variant: int | None = None) -> torch.Tensor:
-    """Causal varlen attention over packed prompts (variant 0: tcgen05 kernel
-    for head_dim 128; 1: mma.sync kernel)."""
+    """Causal varlen attention over packed prompts.  variant 0 (default,
+    ``SSB_PREFILL_ATTN_VARIANT``): persistent tcgen05 kernel for head_dim 128
+    (two query heads per CTA when the GQA group is even); 1: mma.sync kernel;
+    2: tcgen05 kernel with one CTA per (query tile, head, sequence)."""
     if variant is None:  # SSB_PREFILL_ATTN_VARIANT: A/B switch of the kernel variant
         variant = _PREFILL_VARIANT
     _check(qkv, "qkv")
