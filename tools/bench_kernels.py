@@ -133,21 +133,25 @@ if __name__ == "__main__" and "--what" in sys.argv and sys.argv[sys.argv.index("
 def bench_decode_attn():
     """Decode attention at the bench shape (8B: 512 sequences, ctx 1152,
     32/8 heads, 32-layer pool of 64-token blocks), algorithmic GB/s."""
-    B, nq, nk, d, L, BS, ctx = 512, 32, 8, 128, 32, 64, 1152
+    B, nq, nk, d, BS, ctx = 512, 32, 8, 128, 64, 1152
+    L = int(os.environ.get("DEC_LAYERS", "32"))
+    seq_tables = os.environ.get("DEC_SEQ", "0") == "1"
     nb = B * (ctx // BS + 2)
     pool = torch.empty(nb * L * 2 * nk * BS * d, dtype=torch.bfloat16, device="cuda")
     pool.view(torch.int16)[:: 1 << 20].zero_()
-    tables = torch.randperm(nb, device="cuda", dtype=torch.int64)[: B * (ctx // BS + 2)].to(torch.int32).view(B, -1)
+    ids = torch.arange(nb, device="cuda") if seq_tables else torch.randperm(nb, device="cuda", dtype=torch.int64)
+    tables = ids[: B * (ctx // BS + 2)].to(torch.int32).view(B, -1)
     ctxs = torch.full((B,), ctx, dtype=torch.int32, device="cuda")
     qkv = torch.randn(B, (nq + 2 * nk) * d, device="cuda").to(torch.bfloat16)
     out = torch.empty(B, nq * d, dtype=torch.bfloat16, device="cuda")
-    layer = 17
+    layer = min(17, L - 1)
     ms = timed(lambda: ops.decode_attention(qkv, nq, nk, pool, (L, nk, BS, d), nb, layer, tables, ctxs, out,
                                             d ** -0.5), iters=30, flush=False)
     gb = B * ctx * 2 * nk * d * 2 / 1e9
     print(json.dumps({"what": "decode_attn", "ms": ms, "gbs": gb / ms * 1e3,
                       "stages": os.environ.get("SSB_DECODE_STAGES", "3"), "ctas": os.environ.get("SSB_DECODE_CTAS", "0"),
-                      "variant": os.environ.get("SSB_DECODE_ATTN_VARIANT", "0")}), flush=True)
+                      "variant": os.environ.get("SSB_DECODE_ATTN_VARIANT", "0"), "layers": L,
+                      "sequential_blocks": seq_tables}), flush=True)
 
 
 if __name__ == "__main__" and "--what" in sys.argv and sys.argv[sys.argv.index("--what") + 1] == "decode":
