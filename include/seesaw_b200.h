@@ -138,6 +138,19 @@ int ssb_kv_reshard_unpack(void* pool, ssb_kv_geometry geo, const int32_t* block_
                           const int32_t* nh, const int64_t* off_bytes, const void* staging,
                           void* stream);
 
+/* Fused pack + transfer over peer memory: the same per-peer rectangles as
+ * ssb_kv_reshard_pack, but peer p's rectangle is stored straight to the
+ * device address dst_addr[p] (+ its position in the chunk) -- the peer's
+ * receive buffer mapped into this process over NVLink (CUDA IPC) -- so the
+ * copy into a send staging buffer and the separate all-to-all disappear.
+ * The caller orders the kernel against the peers' use of their buffers
+ * (barrier before: peers finished unpacking the previous chunk; barrier
+ * after: every peer's stores landed) and then runs ssb_kv_reshard_unpack on
+ * its own receive buffer. */
+int ssb_kv_reshard_pack_p2p(const void* pool, ssb_kv_geometry geo, const int32_t* block_ids, int n_ids,
+                            int n_peers, const int32_t* l0, const int32_t* nl, const int32_t* h0,
+                            const int32_t* nh, const int64_t* dst_addr, void* stream);
+
 /* ------------------------------------------------------------------------
  * Batched 2-D strided byte copy: weight column/row re-partition
  * (replaces weight_reload_plan, reshard.py:125-148, charged at

@@ -66,6 +66,7 @@ SIGNATURES: dict[str, list] = {
     "ssb_gemm_lm_head_argmax": [_P, _P, _I, _I, _I, _I, _I, _I, _P, _I, _I, _P, _I64, _P],
     "ssb_argmax_keys_decode": [_P, _I, _P, _P, _P],
     "ssb_kv_reshard_pack": [_P, KVGeometry, _P, _I, _I, _PI32, _PI32, _PI32, _PI32, _PI64, _P, _P],
+    "ssb_kv_reshard_pack_p2p": [_P, KVGeometry, _P, _I, _I, _PI32, _PI32, _PI32, _PI32, _PI64, _P],
     "ssb_kv_reshard_unpack": [_P, KVGeometry, _P, _I, _I, _PI32, _PI32, _PI32, _PI32, _PI64, _P, _P],
     "ssb_copy2d_batched": [_P, _P, _P, _I, _I64, _P],
     "ssb_init_weights": [_P, _P, _I, _I64, ctypes.c_uint64, _P],

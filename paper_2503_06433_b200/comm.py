@@ -59,6 +59,12 @@ class Comm:
         shared host KV tier).  Collective."""
         raise NotImplementedError
 
+    def peer_addresses(self, t: torch.Tensor) -> list[int]:
+        """Device addresses, valid in THIS process, of every member's ``t``
+        (the tensor each member passes): the local pointer for self, CUDA IPC
+        mappings (NVLink peer memory) for the others.  Collective."""
+        raise NotImplementedError
+
 
 def _pinned(nbytes: int) -> torch.Tensor:
     return torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=torch.cuda.is_available())
@@ -94,6 +100,9 @@ class SoloComm(Comm):
 
     def share_host_buffer(self, nbytes: int) -> torch.Tensor:
         return _pinned(nbytes)
+
+    def peer_addresses(self, t: torch.Tensor) -> list[int]:
+        return [t.data_ptr()]
 
 
 class TorchComm(Comm):
@@ -186,7 +195,27 @@ class TorchComm(Comm):
         return buf
 
 
+    def peer_addresses(self, t: torch.Tensor) -> list[int]:
+        """CUDA IPC: every member exports its allocation, the others map it
+        (cudaIpcOpenMemHandle through torch's shared-storage path)."""
+        storage = t.untyped_storage()
+        handle = storage._share_cuda_()
+        mine = (handle, t.storage_offset() * t.element_size())
+        objs: list = [None] * self.size
+        self._dist.all_gather_object(objs, mine, group=self.group)
+        addrs = []
+        for r, (h, off) in enumerate(objs):
+            if r == self.rank:
+                addrs.append(t.data_ptr())
+                continue
+            peer = torch.UntypedStorage._new_shared_cuda(*h)
+            _IPC_KEEPALIVE.append(peer)
+            addrs.append(peer.data_ptr() + off)
+        return addrs
+
+
 _GROUPS: dict[tuple[int, ...], object] = {}
+_IPC_KEEPALIVE: list = []
 _SHM_KEEPALIVE: list = []
 
 
@@ -315,6 +344,11 @@ class ThreadComm(Comm):
         buf = objs[0]
         self._done()
         return buf
+
+    def peer_addresses(self, t: torch.Tensor) -> list[int]:
+        objs = self._exchange(t.data_ptr())
+        self._done()
+        return list(objs)
 
     def subgroup(self, members) -> Comm:
         members = tuple(members)

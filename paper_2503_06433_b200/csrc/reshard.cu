@@ -184,17 +184,19 @@ __global__ void __launch_bounds__(32) kv_reshard_bulk_kernel(
   bulk_wait<0>();
 }
 
+// staging == nullptr with `absolute`: off[p] are absolute device addresses
+// (peer memory mapped over NVLink for the P2P pack; see ssb_kv_reshard_pack_p2p).
 int kv_reshard(bool pack, void* pool, ssb_kv_geometry geo, const int32_t* ids, int n_ids, int n_peers,
                const int32_t* l0, const int32_t* nl, const int32_t* h0, const int32_t* nh,
-               const int64_t* off, void* staging, void* stream) {
+               const int64_t* off, void* staging, void* stream, bool absolute = false) {
   SSB_REQUIRE(n_peers > 0 && n_peers <= SSB_MAX_PEERS, "kv_reshard: n_peers=%d out of range", n_peers);
   SSB_REQUIRE(geo.n_layers > 0 && geo.n_heads > 0 && geo.block_size > 0 && geo.head_dim > 0,
               "kv_reshard: bad geometry");
   SSB_REQUIRE(n_ids >= 0, "kv_reshard: n_ids < 0");
   if (n_ids == 0) return 0;
-  SSB_REQUIRE(pool && staging && ids, "kv_reshard: null pointer");
+  SSB_REQUIRE(pool && (staging || absolute) && ids, "kv_reshard: null pointer");
   if ((static_cast<int64_t>(geo.block_size) * geo.head_dim * 2) % 16 != 0 || !aligned16(pool) ||
-      !aligned16(staging)) {
+      (!absolute && !aligned16(staging))) {
     set_error("kv_reshard: head plane and buffers must be 16-byte aligned");
     return SSB_EALIGN;
   }
@@ -234,7 +236,8 @@ int kv_reshard(bool pack, void* pool, ssb_kv_geometry geo, const int32_t* ids, i
   }();
   bool single_head = true;
   for (int p = 0; p < n_peers; ++p) single_head = single_head && (t.nh[p] <= 1);
-  const bool bulk = bulk_env >= 0 ? bulk_env != 0 : (pack && single_head && t.uniform_nl > 0);
+  // peer-memory stores go through the LSU path (plain st.global to UVA peer addresses)
+  const bool bulk = !absolute && (bulk_env >= 0 ? bulk_env != 0 : (pack && single_head && t.uniform_nl > 0));
   if (bulk) {
     const int smem = kBulkSlots * kBulkChunk;
     static bool attr = false;
@@ -397,3 +400,10 @@ int ssb_copy2d_batched(const void* src, void* dst, const ssb_copy_desc* descs, i
 }
 
 }  // extern "C"
+
+extern "C" int ssb_kv_reshard_pack_p2p(const void* pool, ssb_kv_geometry geo, const int32_t* block_ids, int n_ids,
+                                       int n_peers, const int32_t* l0, const int32_t* nl, const int32_t* h0,
+                                       const int32_t* nh, const int64_t* dst_addr, void* stream) {
+  return ssb::kv_reshard(true, const_cast<void*>(pool), geo, block_ids, n_ids, n_peers, l0, nl, h0, nh, dst_addr,
+                         nullptr, stream, true);
+}

@@ -111,6 +111,19 @@ def kv_reshard_unpack(pool, geometry, block_ids, peers, staging) -> None:
     _kv_reshard("ssb_kv_reshard_unpack", pool, geometry, block_ids, peers, staging)
 
 
+def kv_reshard_pack_p2p(pool, geometry, block_ids, peers) -> None:
+    """pool -> every peer's receive buffer directly (peer memory): ``peers``
+    are (l0, nl, h0, nh, absolute destination address) per peer."""
+    if not pool.is_cuda or not block_ids.is_cuda or block_ids.dtype != torch.int32:
+        raise ValueError("kv_reshard_pack_p2p: CUDA pool and int32 CUDA block ids required")
+    geo = _lib.KVGeometry(*geometry)
+    arrs = [_lib.int32_array(p[i] for p in peers) for i in range(4)]
+    dst = _lib.int64_array(p[4] for p in peers)
+    call("ssb_kv_reshard_pack_p2p", pool.data_ptr(), geo, block_ids.data_ptr(), block_ids.numel(), len(peers),
+         *[ctypes.cast(a, ctypes.POINTER(ctypes.c_int32)) for a in arrs], ctypes.cast(dst, ctypes.POINTER(ctypes.c_int64)),
+         _stream())
+
+
 def _kv_reshard(name, pool, geometry, block_ids, peers, staging) -> None:
     if not pool.is_cuda or not staging.is_cuda or not block_ids.is_cuda:
         raise ValueError(f"{name}: pool, staging and block ids must be CUDA tensors")

@@ -129,6 +129,8 @@ class Worker:
         self.fuse_argmax = os.environ.get("SSB_FUSE_ARGMAX", "1") != "0"
         # split-K for skinny projections (a workspace per lane)
         self.split_k = os.environ.get("SSB_SPLIT_K", "1") != "0"
+        # KV re-shard with the transfer fused into the pack (peer memory)
+        self.p2p_reshard = os.environ.get("SSB_RESHARD_P2P", "0") == "1"
 
     # ------------------------------------------------------------ layouts --
     def _tp_comm(self, cfg: ParallelismConfig, stage: int) -> Comm:
@@ -232,6 +234,8 @@ class Worker:
         ids_all = np.asarray(block_ids, dtype=np.int32)
         if ids_all.size == 0:
             return 0
+        if self.p2p_reshard and self.device.type == "cuda" and self.per_replica > 1:
+            return self._reshard_kv_p2p(model, src_cfg, dst_cfg, geo_s, geo_d, ids_all, chunk_blocks, cell)
         max_cells_s = sum(r.cells for r in ex.send)
         max_cells_r = sum(r.cells for r in ex.recv)
         chunk = min(chunk_blocks, ids_all.size)
@@ -294,6 +298,51 @@ class Worker:
             ids, _, r_peers, _, _, _ = chunks[i]
             main.wait_event(arrived[i])
             ops.kv_reshard_unpack(self.pool, geo_d.as_tuple(), ids, r_peers, recvs[i % nbuf])
+        return sent
+
+    def _reshard_kv_p2p(self, model, src_cfg, dst_cfg, geo_s, geo_d, ids_all, chunk_blocks, cell) -> int:
+        """KV re-shard with the transfer fused into the pack: every rank's
+        pack kernel stores each peer's rectangles straight into that peer's
+        receive buffer (CUDA IPC peer memory over NVLink), then each rank
+        unpacks its own buffer.  Per chunk: barrier (peers finished unpacking
+        the previous chunk) -> pack_p2p -> barrier (all stores landed) ->
+        unpack.  No send staging, no NCCL.  (SSB_RESHARD_P2P=1; not the
+        default until measured on NVLink.)"""
+        P, me = self.per_replica, self.gpu
+        ex = [kv_exchange(model, src_cfg, dst_cfg, g) for g in range(P)]
+        chunk = min(chunk_blocks, ids_all.size)
+        # identical on every rank: the buffer every rank allocates and maps
+        recv_cells = max(sum(r.cells for r in e.recv) for e in ex)
+        key = (src_cfg, dst_cfg, chunk, recv_cells)
+        if getattr(self, "_p2p", None) is None or self._p2p[0] != key:
+            recv = torch.empty(chunk * recv_cells * cell + 8, dtype=torch.bfloat16, device=self.device)
+            self._p2p = (key, recv, self.replica_comm.peer_addresses(recv))
+        _, recv, addrs = self._p2p
+        stream = torch.cuda.current_stream(self.device)
+        sent = 0
+        for c0 in range(0, ids_all.size, chunk):
+            ids_np = ids_all[c0 : c0 + chunk]
+            nid = int(ids_np.size)
+            ids = torch.from_numpy(ids_np).to(self.device)
+            peers = []
+            for q in range(P):
+                rs = ex[me].send[q]
+                # my section in q's buffer follows the sections of ranks < me
+                off = 2 * sum(nid * ex[p].send[q].cells * cell for p in range(me))
+                peers.append((rs.l0, rs.nl, rs.h0, rs.nh, addrs[q] + off))
+                if q != me:
+                    sent += 2 * nid * rs.cells * cell
+            stream.synchronize()
+            self.replica_comm.barrier()  # every peer finished reading its buffer
+            ops.kv_reshard_pack_p2p(self.pool, geo_s.as_tuple(), ids, peers)
+            stream.synchronize()
+            self.replica_comm.barrier()  # every rank's stores into my buffer landed
+            r_peers, roff = [], 0
+            for p in range(P):
+                rr = ex[me].recv[p]
+                r_peers.append((rr.l0, rr.nl, rr.h0, rr.nh, 2 * roff))
+                roff += nid * rr.cells * cell
+            ops.kv_reshard_unpack(self.pool, geo_d.as_tuple(), ids, r_peers, recv)
         return sent
 
     # ------------------------------------------------------------- forward --

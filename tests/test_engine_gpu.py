@@ -64,7 +64,7 @@ def run_threads(n, fn):
     return out
 
 
-def _run_tiny(arch_name: str, cfg_p, cfg_d, n_req=8, s_in=64, s_out=32, gpu_seqs=None):
+def _run_tiny(arch_name: str, cfg_p, cfg_d, n_req=8, s_in=64, s_out=32, gpu_seqs=None, p2p=False):
     arch = PRESETS[arch_name]
     model = arch.model_spec()
     W = cfg_p.num_gpus
@@ -86,6 +86,7 @@ def _run_tiny(arch_name: str, cfg_p, cfg_d, n_req=8, s_in=64, s_out=32, gpu_seqs
     def body(r):
         dev = torch.device("cuda", 0)
         wk = Worker(arch, comms[r], cfg_p.dp, dev, seed=0, max_pos=256)
+        wk.p2p_reshard = p2p
 
         def before(w, blocks, cfg_to):
             snaps[(r, "pool_before", cfg_to)] = (w.pool.detach().cpu().clone(), blocks.copy(), w.state.cfg)
@@ -141,8 +142,15 @@ def test_weights_bit_exact_after_repartition(tiny_run):
                 np.testing.assert_array_equal(got, exp, err_msg=f"rank {r} {t.key} {s.logical}")
 
 
-def test_kv_pool_bit_exact_after_reshard(tiny_run):
-    arch, _, _, _, snaps = tiny_run
+@pytest.fixture(scope="module")
+def tiny_run_p2p(cuda):
+    # the KV re-shard with the transfer fused into the pack (peer-memory stores)
+    return _run_tiny("tiny", ParallelismConfig(1, 2, 1), ParallelismConfig(2, 1, 1), p2p=True)
+
+
+@pytest.mark.parametrize("which", ["nccl_path", "p2p_path"])
+def test_kv_pool_bit_exact_after_reshard(tiny_run, tiny_run_p2p, which):
+    arch, _, _, _, snaps = tiny_run if which == "nccl_path" else tiny_run_p2p
     cfg_d = ParallelismConfig(2, 1, 1)
     before = [snaps[(r, "pool_before", cfg_d)] for r in range(2)]
     blocks = before[0][1]
@@ -195,6 +203,14 @@ def check_greedy(arch, reqs, prompts, outputs, tp_prefill, tp_decode):
 def test_greedy_tokens_match_oracle(tiny_run):
     arch, reqs, prompts, res, _ = tiny_run
     check_greedy(arch, reqs, prompts, res[0][0].outputs, 1, 2)
+
+
+def test_p2p_reshard_same_tokens_and_bytes(tiny_run, tiny_run_p2p):
+    """The peer-memory re-shard yields the same run: tokens, replay, bytes."""
+    a, b = tiny_run[3][0][0], tiny_run_p2p[3][0][0]
+    assert a.outputs == b.outputs
+    assert replay_check(b)
+    assert a.measured["kv_bytes_sent"] == b.measured["kv_bytes_sent"] > 0
 
 
 def test_logits_within_bf16_tolerance(tiny_run):

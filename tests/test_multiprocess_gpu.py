@@ -26,7 +26,7 @@ import torch.multiprocessing as mp
 pytestmark = pytest.mark.gpu
 
 
-def _rank(rank: int, port: int, outdir: str, tiered: bool) -> None:
+def _rank(rank: int, port: int, outdir: str, tiered: bool, p2p: bool = False) -> None:
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -57,6 +57,7 @@ def _rank(rank: int, port: int, outdir: str, tiered: bool) -> None:
     prompts = synthetic_prompts(reqs, arch.vocab)
     comm = TorchComm()
     wk = Worker(arch, comm, 1, dev, seed=0, max_pos=256)
+    wk.p2p_reshard = p2p
     rep = execute(model, hw, reqs, SchedulingPolicy.TRANSITION_MINIMIZING, ParallelismConfig(1, 2, 1),
                   ParallelismConfig(2, 1, 1), arch=arch, prompts=prompts, comm=comm, device=dev, worker=wk)
     torch.cuda.synchronize()
@@ -77,15 +78,17 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("tiered", [False, True])
-def test_two_process_pp2_tp2(cuda, tiered):
+@pytest.mark.parametrize("tiered,p2p", [(False, False), (True, False), (False, True)])
+def test_two_process_pp2_tp2(cuda, tiered, p2p):
+    """(p2p: the KV re-shard's pack kernel stores straight into the other
+    process's receive buffer through a CUDA IPC mapping.)"""
     from paper_2503_06433_b200 import PRESETS
     from paper_2503_06433_b200.engine import synthetic_prompts
     from paper_2503_06433_b200.specs import Request
     from test_engine_gpu import check_greedy
 
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_rank, args=(_free_port(), d, tiered), nprocs=2, join=True)
+        mp.spawn(_rank, args=(_free_port(), d, tiered, p2p), nprocs=2, join=True)
         res = [pickle.load(open(f"{d}/rank{r}.pkl", "rb")) for r in range(2)]
     for r in res:
         assert r["replay"] and r["transitions"] == 1 and r["host_tier"] == tiered
