@@ -167,7 +167,9 @@ typedef struct ssb_copy_desc {
   int32_t row_bytes;
 } ssb_copy_desc;
 
-/* total_bytes = sum of rows*row_bytes = cum_bytes[n-1] + last size. */
+/* total_bytes = sum of rows*row_bytes = cum_bytes[n-1] + last size.
+ * dst == NULL: every dst_off is an absolute device address (e.g. a peer's
+ * receive buffer mapped over NVLink), the weight re-partition's P2P path. */
 int ssb_copy2d_batched(const void* src, void* dst, const ssb_copy_desc* descs, int n_desc,
                        int64_t total_bytes, void* stream);
 

@@ -387,8 +387,9 @@ int ssb_copy2d_batched(const void* src, void* dst, const ssb_copy_desc* descs, i
   using namespace ssb;
   SSB_REQUIRE(n_desc >= 0 && total_bytes >= 0, "ssb_copy2d_batched: negative sizes");
   if (n_desc == 0 || total_bytes == 0) return 0;
-  SSB_REQUIRE(src && dst && descs, "ssb_copy2d_batched: null pointer");
-  if (!aligned16(src) || !aligned16(dst) || total_bytes % 16) {
+  // dst == NULL: dst_off are absolute device addresses (peer memory)
+  SSB_REQUIRE(src && descs, "ssb_copy2d_batched: null pointer");
+  if (!aligned16(src) || (dst && !aligned16(dst)) || total_bytes % 16) {
     set_error("ssb_copy2d_batched: bases and sizes must be 16-byte aligned");
     return SSB_EALIGN;
   }

@@ -153,17 +153,18 @@ def _kv_reshard(name, pool, geometry, block_ids, peers, staging) -> None:
     )
 
 
-def copy2d_batched(src: torch.Tensor, dst: torch.Tensor, descs: torch.Tensor, total_bytes: int) -> None:
+def copy2d_batched(src: torch.Tensor, dst: torch.Tensor | None, descs: torch.Tensor, total_bytes: int) -> None:
     """Batched strided copy; ``descs`` is a CUDA int64 tensor [n, 6] of
-    (src_off, dst_off, src_stride, dst_stride, cum_bytes, rows | row_bytes<<32)."""
-    if not (src.is_cuda and dst.is_cuda and descs.is_cuda):
+    (src_off, dst_off, src_stride, dst_stride, cum_bytes, rows | row_bytes<<32).
+    ``dst=None``: dst_off are absolute device addresses (peer memory)."""
+    if not (src.is_cuda and (dst is None or dst.is_cuda) and descs.is_cuda):
         raise ValueError("copy2d_batched: CUDA tensors required")
     if descs.dtype != torch.int64 or descs.dim() != 2 or descs.shape[1] != 6:
         raise ValueError("copy2d_batched: descs must be int64 [n, 6]")
     call(
         "ssb_copy2d_batched",
         src.data_ptr(),
-        dst.data_ptr(),
+        dst.data_ptr() if dst is not None else None,
         descs.data_ptr(),
         descs.shape[0],
         total_bytes,

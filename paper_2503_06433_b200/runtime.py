@@ -206,13 +206,35 @@ class Worker:
                 recv_entries.append((r_pos * 2, p.dst_off * 2, p.cols * 2, p.dst_ld * 2, p.rows, p.cols * 2))
                 r_pos += p.numel
             recv_splits.append(r_pos - start)
-        send = torch.empty(max(s_pos, 8), dtype=torch.bfloat16, device=self.device)
         recv = torch.empty(max(r_pos, 8), dtype=torch.bfloat16, device=self.device)
-        sd, stot = _copy_desc_rows(send_entries)
         rd, rtot = _copy_desc_rows(recv_entries)
-        if stot:
-            ops.copy2d_batched(old.arena, send, torch.from_numpy(sd).to(self.device), stot)
-        self.replica_comm.all_to_all(recv, send, recv_splits, send_splits)
+        if self.p2p_reshard and self.device.type == "cuda" and n > 1:
+            # pack + transfer in one kernel: every piece is stored straight into
+            # its owner's receive buffer (IPC peer memory), at the section that
+            # follows the sections of the ranks before this one
+            addrs = self.replica_comm.peer_addresses(recv)
+            p2p_entries = []
+            for q in range(n):
+                base = sum(pc.numel for p in range(self.gpu)
+                           for pc in repartition_pieces(old_layouts[p], new_layouts[q]))
+                for pc in repartition_pieces(old_layouts[self.gpu], new_layouts[q]):
+                    p2p_entries.append((pc.src_off * 2, addrs[q] + base * 2, pc.src_ld * 2, pc.cols * 2, pc.rows,
+                                        pc.cols * 2))
+                    base += pc.numel
+            pd, ptot = _copy_desc_rows(p2p_entries)
+            stream = torch.cuda.current_stream(self.device)
+            stream.synchronize()
+            self.replica_comm.barrier()  # every receive buffer exists and is idle
+            if ptot:
+                ops.copy2d_batched(old.arena, None, torch.from_numpy(pd).to(self.device), ptot)
+            stream.synchronize()
+            self.replica_comm.barrier()  # every piece landed
+        else:
+            send = torch.empty(max(s_pos, 8), dtype=torch.bfloat16, device=self.device)
+            sd, stot = _copy_desc_rows(send_entries)
+            if stot:
+                ops.copy2d_batched(old.arena, send, torch.from_numpy(sd).to(self.device), stot)
+            self.replica_comm.all_to_all(recv, send, recv_splits, send_splits)
         if rtot:
             ops.copy2d_batched(recv, new.arena, torch.from_numpy(rd).to(self.device), rtot)
         self.state = new

@@ -149,6 +149,16 @@ def tiny_run_p2p(cuda):
 
 
 @pytest.mark.parametrize("which", ["nccl_path", "p2p_path"])
+def test_weights_bit_exact_after_repartition_both_paths(tiny_run, tiny_run_p2p, which):
+    snaps = (tiny_run if which == "nccl_path" else tiny_run_p2p)[4]
+    ref = tiny_run[4]
+    for r in range(2):
+        got, _ = snaps[(r, "arena_after", ParallelismConfig(2, 1, 1))]
+        exp, _ = ref[(r, "arena_after", ParallelismConfig(2, 1, 1))]
+        assert torch.equal(got.view(torch.int16), exp.view(torch.int16))
+
+
+@pytest.mark.parametrize("which", ["nccl_path", "p2p_path"])
 def test_kv_pool_bit_exact_after_reshard(tiny_run, tiny_run_p2p, which):
     arch, _, _, _, snaps = tiny_run if which == "nccl_path" else tiny_run_p2p
     cfg_d = ParallelismConfig(2, 1, 1)
