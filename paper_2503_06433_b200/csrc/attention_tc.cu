@@ -907,8 +907,11 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
     uint32_t t = 0, ic = 0;
     PairIter it(blockIdx.x, gridDim.x, n_items, n_qt_max, pairs, nseq, cu);
     while (it.next()) {
-      const int n_kv = it.qt + 1;
-      const int qrow = it.qt * kT + r;
+      // item fields as scalars (kept in registers, not re-read from the
+      // iterator's local-memory copy in the epilogue)
+      const int qt = it.qt, len = it.len, start = it.start, pair = it.pair;
+      const int n_kv = qt + 1;
+      const int qrow = qt * kT + r;
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < n_kv; ++j, ++t) {
         // S(t) ready; pipe order also means every earlier P.V of this head is done (O stable)
@@ -924,10 +927,10 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
           for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(v[i]) * scale_log2;
         }
         const int k0 = j * kT;
-        if (j == it.qt || k0 + kT > it.len) {
+        if (j == qt || k0 + kT > len) {
 #pragma unroll
           for (int i = 0; i < kT; ++i)
-            if (k0 + i > qrow || k0 + i >= it.len) sv[i] = -INFINITY;
+            if (k0 + i > qrow || k0 + i >= len) sv[i] = -INFINITY;
         }
         float mx = -INFINITY;
 #pragma unroll
@@ -973,14 +976,14 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
       // epilogue: O / l of this head, then hand O back to the MMA warp
       mbar_wait(&o_done[hh], ic & 1);
       tc_fence_after();
-      const float inv = l > 0.f ? 1.f / l : 0.f;
-      __nv_bfloat16* orow = out + static_cast<size_t>(it.start + qrow) * ldo + (2 * it.pair + hh) * kD;
+      const float inv = l > 0.f ? __frcp_rn(l) : 0.f;
+      __nv_bfloat16* orow = out + static_cast<size_t>(start + qrow) * ldo + (2 * pair + hh) * kD;
 #pragma unroll 1
       for (int c = 0; c < kD / 32; ++c) {
         uint32_t v[32];
         tmem_ld32(o_acc + c * 32, v);
         tmem_ld_wait();
-        if (qrow < it.len) {
+        if (qrow < len) {
           uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
