@@ -348,3 +348,31 @@ def test_ragged_lengths_llama_shape_single_gpu(cuda):
         if a[0] != b[0]:
             top = torch.topk(pre1[i], 2).values
             assert float(top[0] - top[1]) < 0.05 * scale, (r.id, a[0], b[0])
+
+
+@pytest.mark.parametrize("n,cpu_seqs,gpu_res", [(8, 3, 0), (5, 2, 0), (7, 7, 0), (1, 1, 0), (9, 2, 2), (10, 3, 1)])
+def test_transition_law_matches_reference(cuda, n, cpu_seqs, gpu_res):
+    """Schedule parity with the reference's transition law
+    (pkg/tests/test_sim.py:104-117: transitions == 2*ceil(n/cpu_seqs) - 1 when
+    every prefilled sequence rides the CPU tier).  With a GPU tier that holds
+    only the prefill reserve, the engine's P-phases are CPU-bound exactly like
+    the reference's; with `gpu_res` extra resident slots the native-mode law
+    is 2*ceil(n/(gpu_res + cpu_seqs)) - 1 (KV that fits in HBM stays there)."""
+    from paper_2503_06433_b200.comm import SoloComm
+    from paper_2503_06433_b200.specs import kv_bytes_per_token, total_weight_bytes
+
+    arch = PRESETS["tiny"]
+    model = arch.model_spec()
+    s_in, s_out = 16, 3
+    k = (s_in + s_out) * kv_bytes_per_token(model)
+    hw = tiny_hw(1, gpu_memory=total_weight_bytes(model) + (1 + gpu_res) * k, host_memory_per_gpu=cpu_seqs * k)
+    reqs = [Request(i, s_in, s_out) for i in range(n)]
+    prompts = synthetic_prompts(reqs, arch.vocab)
+    dev = torch.device("cuda", 0)
+    wk = Worker(arch, SoloComm(), 1, dev, seed=0, max_pos=64)
+    cfg = ParallelismConfig(1, 1, 1)
+    rep = execute(model, hw, reqs, SchedulingPolicy.TRANSITION_MINIMIZING, cfg, cfg, arch=arch, prompts=prompts,
+                  comm=SoloComm(), device=dev, worker=wk, max_prefill_tokens=s_in)
+    assert replay_check(rep), replay_check(rep).violation
+    assert rep.transitions == 2 * -(-n // (gpu_res + cpu_seqs)) - 1
+    assert all(len(rep.outputs[r.id]) == s_out for r in reqs)
