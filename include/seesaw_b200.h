@@ -18,6 +18,7 @@
 #ifndef SEESAW_B200_H_
 #define SEESAW_B200_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -227,6 +228,32 @@ int ssb_init_weights(void* arena, const ssb_init_seg* segs, int n_seg, int64_t t
  * prompt before the LM head) */
 int ssb_rmsnorm(const void* x, int ldx, const int32_t* row_idx, const void* w, void* out, int ldo,
                 int rows, int hidden, float eps, void* stream);
+
+/* ------------------------------------------------------------------------
+ * TP combine over NVLink peer memory fused with the following RMSNorm
+ * (replaces the NCCL all-reduce of the row-parallel o_proj / down_proj
+ * partials that the reference charges per layer, perf.py:71-74 /
+ * SURVEY.md §8(e), plus the rmsnorm launch after it).
+ *
+ * Every *_addrs argument is a HOST array of nranks device addresses valid in
+ * the calling process (own buffer at [rank], CUDA IPC mappings of the peers'
+ * buffers elsewhere; comm.peer_addresses):
+ *   part[r]  bf16 [rows, ld]  rank r's partial sums (rank 0's include the residual)
+ *   x[r]     bf16 [rows, ld]  receives x = sum_r part[r] (fp32 sum in rank order, bf16)
+ *   h[r]     bf16 [rows, ld]  receives rmsnorm(x) * gamma   (h_addrs/gamma may be NULL)
+ *   sig[r]   ssb_tp_signal_bytes() of zero-initialised device memory per rank
+ * Rank r reduces rows [r*rows/n, (r+1)*rows/n) and stores them to every rank.
+ * All ranks must make the same calls with the same (rows, hidden, ld,
+ * max_blocks) and a per-call epoch that starts at 1 and grows by one; the
+ * call synchronises with the peers on the device (no host round trip).  A
+ * peer missing for 30 s sets *err = 1 (traps if err is NULL).
+ * hidden <= 8192, nranks <= 8.
+ * ---------------------------------------------------------------------- */
+size_t ssb_tp_signal_bytes(void);
+int ssb_tp_allreduce_rmsnorm(const uint64_t* part_addrs, const uint64_t* x_addrs, const uint64_t* h_addrs,
+                             const uint64_t* sig_addrs, int nranks, int rank, int rows, int hidden, int ld,
+                             const void* gamma, float eps, uint32_t epoch, int max_blocks, uint32_t* err,
+                             void* stream);
 
 /* Decode-step bookkeeping on device: ctx_lens[b] += 1; positions[b] =
  * ctx_lens[b]-1; slots[b] = block_tables[b][pos/bs]*bs + pos%bs. */

@@ -56,6 +56,7 @@ _I64 = ctypes.c_int64
 _F = ctypes.c_float
 _PI32 = ctypes.POINTER(ctypes.c_int32)
 _PI64 = ctypes.POINTER(ctypes.c_int64)
+_PU64 = ctypes.POINTER(ctypes.c_uint64)
 
 # name -> argtypes (restype is int for all compute entry points)
 SIGNATURES: dict[str, list] = {
@@ -80,6 +81,8 @@ SIGNATURES: dict[str, list] = {
     "ssb_argmax_combine": [_P, _P, _I, _I, _P, _P],
     "ssb_prefill_attention": [_P, _I, _I, _I, _I, _I, _P, _I, _I, _P, _I, _F, _I, _P],
     "ssb_decode_attention": [_P, _I, _I, _I, _P, KVGeometry, _I, _I, _P, _I, _P, _I, _P, _I, _F, _P],
+    "ssb_tp_allreduce_rmsnorm": [_PU64, _PU64, _PU64, _PU64, _I, _I, _I, _I, _I, _P, _F, ctypes.c_uint32, _I, _P,
+                                 _P],
 }
 
 _lock = threading.Lock()
@@ -104,6 +107,8 @@ def load() -> ctypes.CDLL:
             lib.ssb_device_sm_count.restype = ctypes.c_int
             lib.ssb_gemm_plan.restype = ctypes.c_int64
             lib.ssb_gemm_plan.argtypes = [_I, _I, _I, _I, _I, _I64, _PI32]
+            lib.ssb_tp_signal_bytes.restype = ctypes.c_size_t
+            lib.ssb_tp_signal_bytes.argtypes = []
             for name, args in SIGNATURES.items():
                 fn = getattr(lib, name)
                 fn.argtypes = args
@@ -155,3 +160,8 @@ def int32_array(values) -> ctypes.Array:
 def int64_array(values) -> ctypes.Array:
     vals = list(values)
     return (ctypes.c_int64 * max(len(vals), 1))(*vals)
+
+
+def uint64_array(values) -> ctypes.Array:
+    vals = [int(v) for v in values]
+    return (ctypes.c_uint64 * max(len(vals), 1))(*vals)

@@ -329,3 +329,23 @@ def decode_attention(qkv: torch.Tensor, nq: int, nk: int, pool: torch.Tensor, ge
          _lib.KVGeometry(*geometry), num_blocks, layer, block_tables.data_ptr(), block_tables.shape[1],
          ctx_lens.data_ptr(), ctx_lens.numel(), out.data_ptr(), out.stride(0), scale, _stream())
     return out
+
+
+def tp_signal_bytes() -> int:
+    return int(load().ssb_tp_signal_bytes())
+
+
+def tp_allreduce_rmsnorm(part_addrs, x_addrs, h_addrs, sig_addrs, rank: int, rows: int, hidden: int,
+                         gamma: torch.Tensor | None, eps: float, epoch: int, max_blocks: int,
+                         err: torch.Tensor | None = None) -> None:
+    """x = sum over ranks of part, h = rmsnorm(x) * gamma, written into every
+    rank's x / h over NVLink peer memory (C-ABI ssb_tp_allreduce_rmsnorm).
+    The address lists are this process's view of every rank's buffers
+    (comm.peer_addresses)."""
+    n = len(part_addrs)
+    if gamma is not None:
+        _check(gamma, "gamma")
+    call("ssb_tp_allreduce_rmsnorm", _lib.uint64_array(part_addrs), _lib.uint64_array(x_addrs),
+         _lib.uint64_array(h_addrs) if h_addrs is not None else None, _lib.uint64_array(sig_addrs), n, rank, rows,
+         hidden, hidden, gamma.data_ptr() if gamma is not None else None, eps, epoch, max_blocks,
+         err.data_ptr() if err is not None else None, _stream())

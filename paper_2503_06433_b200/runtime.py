@@ -131,6 +131,15 @@ class Worker:
         self.split_k = os.environ.get("SSB_SPLIT_K", "1") != "0"
         # KV re-shard with the transfer fused into the pack (peer memory)
         self.p2p_reshard = os.environ.get("SSB_RESHARD_P2P", "0") == "1"
+        # TP combine (all-reduce of the row-parallel partials + the rmsnorm
+        # after it) as one kernel over NVLink peer memory (tpcombine.py).
+        # None = automatic: on for NCCL process groups; ThreadComm ranks need
+        # one CUDA stream per thread for its device-side barrier, so tests
+        # opt in.  SSB_TP_FUSED=0/1 forces it.
+        env = os.environ.get("SSB_TP_FUSED")
+        self.fused_tp: bool | None = None if env is None else env == "1"
+        self.fused_tp_blocks = int(os.environ.get("SSB_TP_FUSED_BLOCKS", "0"))
+        self._tp_arenas: dict = {}
 
     # ------------------------------------------------------------ layouts --
     def _tp_comm(self, cfg: ParallelismConfig, stage: int) -> Comm:
@@ -372,11 +381,49 @@ class Worker:
         wl = self.state.weights
         return range(wl.layer_begin, wl.layer_end)
 
-    def _block(self, x: torch.Tensor, layer: int, attn_fn, buf: dict, rope: tuple, cap: int = 0) -> None:
+    def _arena(self, rows: int):
+        """The fused TP combine's peer arena for this layout (None: use the
+        all-reduce + rmsnorm path).  Collective over the TP group."""
+        st = self.state
+        tp = st.tp_comm
+        if tp.size == 1 or self.device.type != "cuda" or rows == 0:
+            return None
+        use = self.fused_tp
+        if use is None:
+            from .comm import TorchComm
+
+            use = isinstance(tp, TorchComm) and not tp._host_staged
+        if not use:
+            return None
+        from . import tpcombine
+        from .comm import ThreadComm
+
+        blocks = self.fused_tp_blocks or (
+            16 if isinstance(tp, ThreadComm) else torch.cuda.get_device_properties(self.device).multi_processor_count)
+        return tpcombine.get_arena(self._tp_arenas, tp, self.device, self.arch.hidden, rows, blocks)
+
+    def _next_gamma(self, layer: int, final: bool):
+        """The norm gain the combine after ``layer``'s MLP applies: the next
+        layer's attn_norm on this stage, else final_norm when ``final``."""
+        if layer + 1 < self.state.weights.layer_end:
+            return self.w(f"L{layer + 1}.attn_norm")
+        return self.w("final_norm") if final else None
+
+    def _block(self, x: torch.Tensor, layer: int, attn_fn, buf: dict, rope: tuple, cap: int = 0, ar=None,
+               h_ready: bool = False, final: bool = False) -> bool:
         """One transformer layer on x (in place); attn_fn(qkv, layer_local) -> attn out.
         ``rope`` = (positions, slots) of the rows: RoPE and the paged K/V
         append run in the QKV GEMM's epilogue (head_dim 128) or as a separate
-        kernel.  ``cap`` bounds the GEMMs' persistent grid (decode lane overlap)."""
+        kernel.  ``cap`` bounds the GEMMs' persistent grid (decode lane overlap).
+
+        With a peer arena ``ar`` (TP > 1, x = ar.x[:T]) the row-parallel
+        projections write their partials to ar.part and each combine also
+        produces the NEXT rmsnorm (ar.h): ``h_ready`` says this layer's input
+        norm is already in ar.h; returns whether the next one is (the
+        combine after the MLP applies the next layer's attn_norm, or
+        final_norm on the last layer when ``final``)."""
+        if ar is not None:
+            return self._block_fused(x, layer, attn_fn, buf, rope, cap, ar, h_ready, final)
         st = self.state
         eps = self.arch.rms_eps
         p = f"L{layer}."
@@ -400,6 +447,36 @@ class Worker:
         act = ops.gemm(h, self.w(p + "w13"), out=buf["act"], silu_mul=True, max_ctas=cap, workspace=ws)
         ops.gemm(act, self.w(p + "w2"), out=x, residual=x if lead else None, max_ctas=cap, workspace=ws)
         self._reduce_into(x)
+        return False
+
+    def _block_fused(self, x, layer, attn_fn, buf, rope, cap, ar, h_ready, final) -> bool:
+        st = self.state
+        eps = self.arch.rms_eps
+        p = f"L{layer}."
+        lead = st.rank == 0
+        ws = buf["ws"]
+        local = layer - st.weights.layer_begin
+        nq, nk = st.weights.n_q_heads, st.weights.n_kv_heads
+        pos, slots = rope
+        geo = self.geometry().as_tuple()
+        T = x.shape[0]
+        h, part = ar.h[:T], ar.part[:T]
+        if not h_ready:
+            ops.rmsnorm(x, self.w(p + "attn_norm"), eps, out=h)
+        if self.fuse_rope and self.arch.head_dim == 128:
+            qkv = ops.gemm_qkv_rope_kv(h, self.w(p + "wqkv"), buf["qkv"], nq, nk, pos, self.rope_cos, self.rope_sin,
+                                       self.pool, geo, local, slots, max_ctas=cap, workspace=ws)
+        else:
+            qkv = ops.gemm(h, self.w(p + "wqkv"), out=buf["qkv"], max_ctas=cap, workspace=ws)
+            ops.rope_kv_append(qkv, nq, nk, pos, self.rope_cos, self.rope_sin, self.pool, geo, local, slots)
+        attn = attn_fn(qkv, local)
+        ops.gemm(attn, self.w(p + "wo"), out=part, residual=x if lead else None, max_ctas=cap, workspace=ws)
+        ar.combine(T, self.w(p + "mlp_norm"), eps)
+        act = ops.gemm(h, self.w(p + "w13"), out=buf["act"], silu_mul=True, max_ctas=cap, workspace=ws)
+        ops.gemm(act, self.w(p + "w2"), out=part, residual=x if lead else None, max_ctas=cap, workspace=ws)
+        g = self._next_gamma(layer, final)
+        ar.combine(T, g, eps)
+        return g is not None
 
     def _reduce_into(self, x: torch.Tensor) -> None:
         """Row-parallel combine: rank 0 added the residual in its GEMM epilogue,
@@ -476,11 +553,21 @@ class Worker:
         T = int(cu_seqlens[-1])
         n = len(cu_seqlens) - 1
         buf = self._buffers(T)
-        x = torch.empty(T, a.hidden, dtype=torch.bfloat16, device=self.device)
+        ar = self._arena(T)
+        h_ready = False
+        if ar is not None:
+            x = ar.x[:T]
+        else:
+            x = torch.empty(T, a.hidden, dtype=torch.bfloat16, device=self.device)
         if st.stage == 0:
-            ops.embedding(tokens, self.w("embed"), st.weights.vocab_begin, x)
-            if st.tp_comm.size > 1:
-                st.tp_comm.all_reduce_(x)
+            if ar is not None:
+                ops.embedding(tokens, self.w("embed"), st.weights.vocab_begin, ar.part[:T])
+                ar.combine(T, self.w(f"L{st.weights.layer_begin}.attn_norm"), a.rms_eps)
+                h_ready = True
+            else:
+                ops.embedding(tokens, self.w("embed"), st.weights.vocab_begin, x)
+                if st.tp_comm.size > 1:
+                    st.tp_comm.all_reduce_(x)
         else:
             self.replica_comm.recv(x, st.pp_prev)
         pos = np.concatenate([np.arange(cu_seqlens[i + 1] - cu_seqlens[i], dtype=np.int32) for i in range(n)])
@@ -498,7 +585,7 @@ class Worker:
             return ops.prefill_attention(qkv, nq, nk, a.head_dim, cu_d, max_len, buf["attn"], self.scale)
 
         for layer in self._layers():
-            self._block(x, layer, attn, buf, (pos_d, slots_d))
+            h_ready = self._block(x, layer, attn, buf, (pos_d, slots_d), ar=ar, h_ready=h_ready)
         if st.stage < st.cfg.pp - 1:
             self.replica_comm.send(x, st.pp_next)
             return
@@ -536,19 +623,27 @@ class Worker:
         geo = self.geometry()
         nq, nk = st.weights.n_q_heads, st.weights.n_kv_heads
         lanes = []
+        ar = self._arena(spans[0][1] - spans[0][0]) if len(spans) == 1 else None
+        final = st.stage == st.cfg.pp - 1
         for li, ((b0, b1), s) in enumerate(zip(spans, streams)):
             with torch.cuda.stream(s):
                 n = b1 - b0
                 buf = self._buffers(n, lane=li)
-                x = buf.get("x")
-                if x is None or x.shape[0] != n:
-                    x = buf["x"] = torch.empty(n, a.hidden, dtype=torch.bfloat16, device=self.device)
                 v = dict(tok=tokens[b0:b1], ctx=ctx_lens[b0:b1], tab=tables[b0:b1], pos=positions[b0:b1],
-                         slot=slots[b0:b1], out=out_tokens[b0:b1])
+                         slot=slots[b0:b1], out=out_tokens[b0:b1], h_ready=False)
                 ops.decode_positions(v["ctx"], v["tab"], self.block_size, v["pos"], v["slot"])
-                ops.embedding(v["tok"], self.w("embed"), st.weights.vocab_begin, x)
-                if st.tp_comm.size > 1:
-                    st.tp_comm.all_reduce_(x)
+                if ar is not None:
+                    x = ar.x[:n]
+                    ops.embedding(v["tok"], self.w("embed"), st.weights.vocab_begin, ar.part[:n])
+                    ar.combine(n, self.w(f"L{st.weights.layer_begin}.attn_norm"), a.rms_eps)
+                    v["h_ready"] = True
+                else:
+                    x = buf.get("x")
+                    if x is None or x.shape[0] != n:
+                        x = buf["x"] = torch.empty(n, a.hidden, dtype=torch.bfloat16, device=self.device)
+                    ops.embedding(v["tok"], self.w("embed"), st.weights.vocab_begin, x)
+                    if st.tp_comm.size > 1:
+                        st.tp_comm.all_reduce_(x)
 
                 def attn(qkv, layer_local, v=v, buf=buf):
                     return ops.decode_attention(qkv, nq, nk, self.pool, geo.as_tuple(), self.num_blocks,
@@ -558,10 +653,14 @@ class Worker:
         for layer in self._layers():
             for s, x, attn, buf, v in lanes:
                 with torch.cuda.stream(s):
-                    self._block(x, layer, attn, buf, (v["pos"], v["slot"]), cap)
+                    v["h_ready"] = self._block(x, layer, attn, buf, (v["pos"], v["slot"]), cap, ar=ar,
+                                               h_ready=v["h_ready"], final=final)
         for s, x, _, buf, v in lanes:
             with torch.cuda.stream(s):
-                h = ops.rmsnorm(x, self.w("final_norm"), a.rms_eps, out=buf["h"])
+                if ar is not None and v["h_ready"]:
+                    h = ar.h[: x.shape[0]]
+                else:
+                    h = ops.rmsnorm(x, self.w("final_norm"), a.rms_eps, out=buf["h"])
                 self._logits_argmax(h, v["out"], buf["ws"])
         if len(spans) > 1:
             main.wait_stream(self._side)

@@ -272,7 +272,7 @@ def test_host_tier_single_gpu(cuda):
     check_greedy(arch, reqs, prompts, rep.outputs, 1, 1)
 
 
-def _run_ragged(arch_name, cfg_p, cfg_d, lens, gpu_seqs=None, gpu_memory=2e9, record_logits=False):
+def _run_ragged(arch_name, cfg_p, cfg_d, lens, gpu_seqs=None, gpu_memory=2e9, record_logits=False, fused_tp=False):
     """Ragged workload (every request its own input and output length)."""
     from paper_2503_06433_b200.specs import kv_bytes_per_token, total_weight_bytes
 
@@ -290,9 +290,16 @@ def _run_ragged(arch_name, cfg_p, cfg_d, lens, gpu_seqs=None, gpu_memory=2e9, re
 
     def body(r):
         dev = torch.device("cuda", 0)
-        wk = Worker(arch, comms[r], cfg_p.dp, dev, seed=0, max_pos=512)
-        rep = execute(model, hw, reqs, SchedulingPolicy.TRANSITION_MINIMIZING, cfg_p, cfg_d, arch=arch,
-                      prompts=prompts, comm=comms[r], device=dev, worker=wk, record_logits=record_logits)
+        # the fused TP combine's device barrier needs the ranks' kernels to
+        # run concurrently: one stream per virtual rank
+        with torch.cuda.stream(torch.cuda.Stream(dev) if fused_tp else torch.cuda.current_stream(dev)):
+            wk = Worker(arch, comms[r], cfg_p.dp, dev, seed=0, max_pos=512)
+            wk.fused_tp = fused_tp
+            rep = execute(model, hw, reqs, SchedulingPolicy.TRANSITION_MINIMIZING, cfg_p, cfg_d, arch=arch,
+                          prompts=prompts, comm=comms[r], device=dev, worker=wk, record_logits=record_logits)
+            torch.cuda.current_stream(dev).synchronize()
+            if fused_tp:
+                assert wk._tp_arenas and all(a.usable for a in wk._tp_arenas.values())
         return (rep, [x.clone() for x in wk.logit_log]) if record_logits else rep
 
     return arch, reqs, prompts, run_threads(W, body)
@@ -376,3 +383,31 @@ def test_transition_law_matches_reference(cuda, n, cpu_seqs, gpu_res):
     assert replay_check(rep), replay_check(rep).violation
     assert rep.transitions == 2 * -(-n // (gpu_res + cpu_seqs)) - 1
     assert all(len(rep.outputs[r.id]) == s_out for r in reqs)
+
+
+@pytest.mark.parametrize("arch_name,cfg_p,cfg_d", [
+    ("tiny", ParallelismConfig(1, 2, 1), ParallelismConfig(2, 1, 1)),
+    ("tiny", ParallelismConfig(2, 2, 1), ParallelismConfig(4, 1, 1)),
+    ("llama3-8b-2l", ParallelismConfig(2, 1, 1), ParallelismConfig(2, 1, 1)),
+])
+def test_fused_tp_combine_bit_identical(cuda, arch_name, cfg_p, cfg_d):
+    """The fused TP combine (all-reduce + next rmsnorm over peer memory, one
+    kernel) against the all-reduce + rmsnorm path: identical logits and
+    tokens, bit for bit, through TP prefill (embedding combine, varying
+    micro-batch rows, arena growth) and TP decode (shrinking batch)."""
+    import dataclasses
+
+    if arch_name == "llama3-8b-2l":
+        PRESETS[arch_name] = dataclasses.replace(PRESETS["llama3-8b"], num_layers=2, name=arch_name)
+    try:
+        mem = 20e9 if arch_name != "tiny" else 2e9
+        _, reqs, prompts, base = _run_ragged(arch_name, cfg_p, cfg_d, RAGGED, gpu_memory=mem, record_logits=True)
+        _, _, _, fused = _run_ragged(arch_name, cfg_p, cfg_d, RAGGED, gpu_memory=mem, record_logits=True,
+                                     fused_tp=True)
+    finally:
+        if arch_name != "tiny":
+            PRESETS.pop(arch_name, None)
+    (rb, lb), (rf, lf) = base[0], fused[0]
+    assert replay_check(rf), replay_check(rf).violation
+    assert rf.outputs == rb.outputs
+    assert len(lb) == len(lf) and all(torch.equal(a, b) for a, b in zip(lb, lf))
