@@ -422,7 +422,7 @@ def profile_kernels(one, prompts, arch, args, dev, comm, world) -> dict:
         # by phase: decode projections run at M = resident batch (<= prompts),
         # prefill at packed tokens (the prefill LM head at M = prompts of a
         # micro-batch is counted with decode: same skinny shape class)
-        if name in ("ssb_gemm_bf16", "ssb_gemm_bf16_ws"):
+        if name in ("ssb_gemm_bf16", "ssb_gemm_bf16_ws", "ssb_gemm_bf16_rn"):
             M, N, K = a[4], a[5], a[6]
         elif name == "ssb_gemm_qkv_rope_kv":
             M, K = a[3], a[4]

@@ -88,6 +88,31 @@ int ssb_gemm_bf16(const void* A, const void* B, void* C, const void* R, int M, i
 int ssb_gemm_bf16_ws(const void* A, const void* B, void* C, const void* R, int M, int N, int K,
                      int lda, int ldb, int ldc, int ldr, int epilogue, int block_n, int max_ctas,
                      void* workspace, int64_t workspace_bytes, void* stream);
+
+/* RMSNorm folded into the GEMMs around it (single-GPU / TP=1 layout):
+ * rmsnorm(x) * gamma @ W^T == diag(1/rms(x)) * (x @ (W * gamma)^T), so with
+ * the gain folded into the consumer's weights (W[n, k] *= gamma[k]) the
+ * consumer GEMM takes the residual stream x itself as A and scales its
+ * accumulator rows by 1/rms in the epilogue, and the producer of x (the
+ * residual-epilogue GEMM) emits the row sums of squares on the fly: no
+ * rmsnorm launch, no h round trip through HBM.
+ *   ss_out  (SSB_EPI_RESIDUAL only) fp32 [M][ss_parts]: sum of squares of the
+ *           stored bf16 row segment of every N tile; the call writes the
+ *           tile count it used into ss_parts (host side, before returning)
+ *   ss_in   fp32 [M][ss_in_parts] (a producer's ss_out): every epilogue
+ *           scales row m by 1/sqrt(sum_j ss_in[m][j] / hidden + eps) first
+ * Either pointer may be NULL.  */
+typedef struct ssb_rownorm {
+  float* ss_out;
+  const float* ss_in;
+  int ss_in_parts;
+  int hidden;
+  float eps;
+  int ss_parts; /* out */
+} ssb_rownorm;
+int ssb_gemm_bf16_rn(const void* A, const void* B, void* C, const void* R, int M, int N, int K,
+                     int lda, int ldb, int ldc, int ldr, int epilogue, int block_n, int max_ctas,
+                     void* workspace, int64_t workspace_bytes, ssb_rownorm* rn, void* stream);
 /* The configuration block_n = 0 would pick: out_plan[3] = {mode (0 single
  * CTA, 2 CTA pair), N tile, splits (negative: tail split)}; returns the workspace bytes it needs
  * (0 without split-K), <0 on argument error. */
@@ -129,7 +154,7 @@ int ssb_gemm_qkv_rope_kv(const void* A, const void* B, void* qkv, int M, int K, 
                          int nq, int nk, int head_dim, const int32_t* positions, const float* rope_cos,
                          const float* rope_sin, int max_pos, void* pool, ssb_kv_geometry geo,
                          int layer, const int64_t* slots, int block_n, int max_ctas, void* workspace,
-                         int64_t workspace_bytes, void* stream);
+                         int64_t workspace_bytes, ssb_rownorm* rn, void* stream);
 
 int ssb_kv_reshard_pack(const void* pool, ssb_kv_geometry geo, const int32_t* block_ids, int n_ids,
                         int n_peers, const int32_t* l0, const int32_t* nl, const int32_t* h0,
@@ -288,7 +313,7 @@ int ssb_argmax_rows(const float* logits, int ld, int rows, int cols, int index_b
  * Workspace as for ssb_gemm_bf16_ws. */
 int ssb_gemm_lm_head_argmax(const void* A, const void* B, int M, int N, int K, int lda, int ldb,
                             int index_base, unsigned long long* keys, int block_n, int max_ctas,
-                            void* workspace, int64_t workspace_bytes, void* stream);
+                            void* workspace, int64_t workspace_bytes, ssb_rownorm* rn, void* stream);
 /* keys -> (value, index) arrays for ssb_argmax_combine / the token ids. */
 int ssb_argmax_keys_decode(const unsigned long long* keys, int rows, float* out_val, int32_t* out_idx,
                            void* stream);

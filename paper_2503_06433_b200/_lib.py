@@ -50,7 +50,21 @@ class CopyDesc(ctypes.Structure):
     ]
 
 
+class RowNorm(ctypes.Structure):
+    """ssb_rownorm (include/seesaw_b200.h): RMSNorm folded into the GEMMs."""
+
+    _fields_ = [
+        ("ss_out", ctypes.c_void_p),
+        ("ss_in", ctypes.c_void_p),
+        ("ss_in_parts", ctypes.c_int),
+        ("hidden", ctypes.c_int),
+        ("eps", ctypes.c_float),
+        ("ss_parts", ctypes.c_int),
+    ]
+
+
 _P = ctypes.c_void_p
+_PRN = ctypes.POINTER(RowNorm)
 _I = ctypes.c_int
 _I64 = ctypes.c_int64
 _F = ctypes.c_float
@@ -62,9 +76,10 @@ _PU64 = ctypes.POINTER(ctypes.c_uint64)
 SIGNATURES: dict[str, list] = {
     "ssb_gemm_bf16": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P],
     "ssb_gemm_bf16_ws": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _I64, _P],
+    "ssb_gemm_bf16_rn": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _I64, _PRN, _P],
     "ssb_gemm_qkv_rope_kv": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P, KVGeometry, _I, _P,
-                             _I, _I, _P, _I64, _P],
-    "ssb_gemm_lm_head_argmax": [_P, _P, _I, _I, _I, _I, _I, _I, _P, _I, _I, _P, _I64, _P],
+                             _I, _I, _P, _I64, _PRN, _P],
+    "ssb_gemm_lm_head_argmax": [_P, _P, _I, _I, _I, _I, _I, _I, _P, _I, _I, _P, _I64, _PRN, _P],
     "ssb_argmax_keys_decode": [_P, _I, _P, _P, _P],
     "ssb_kv_reshard_pack": [_P, KVGeometry, _P, _I, _I, _PI32, _PI32, _PI32, _PI32, _PI64, _P, _P],
     "ssb_kv_reshard_pack_p2p": [_P, KVGeometry, _P, _I, _I, _PI32, _PI32, _PI32, _PI32, _PI64, _P],

@@ -90,6 +90,13 @@ struct Params {
   RopeKV rk;       // SSB_EPI_ROPE_KV only
   int arg_base;    // SSB_EPI_ARGMAX: global index of accumulator column 0
   int pol_mode;    // L2 cache-policy variant of the operand loads (see producer)
+  // RMSNorm folded into the GEMMs (ssb_rownorm): ss_out[row * tiles_n + tn]
+  // = sum of squares of the stored bf16 row segment (residual epilogue);
+  // ss_in scales every accumulator row by 1/sqrt(sum(ss_in row)/hidden + eps)
+  float* ss_out;
+  const float* ss_in;
+  int ss_in_parts;
+  float ss_hidden, ss_eps;
 };
 
 // Grouped rasterisation: kGroupM tiles of the "band" dimension share one
@@ -127,8 +134,28 @@ __device__ __forceinline__ void unit_decode(const Params& p, int u, int& t, int&
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
 
-// Final epilogue of 32 accumulator columns [col, col+32) of one row.
-__device__ __forceinline__ void store_cols(const Params& p, int row, int col, float (&f)[32]) {
+// 1/rms of row `row` from the producer's per-tile sums of squares, in the
+// rmsnorm kernel's formula (parts summed in order: deterministic).
+__device__ __forceinline__ float row_rms_scale(const Params& p, int row) {
+  const float* src = p.ss_in + static_cast<size_t>(row) * p.ss_in_parts;
+  float ss = 0.f;
+  for (int j = 0; j < p.ss_in_parts; ++j) ss += src[j];
+  return 1.0f / sqrtf(__fadd_rn(__fdiv_rn(ss, p.ss_hidden), p.ss_eps));
+}
+
+__device__ __forceinline__ void scale32(float (&f)[32], float s) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) f[j] = __fmul_rn(f[j], s);
+}
+
+__device__ __forceinline__ float sq_bf16x2(uint32_t v, float ss) {
+  const float a = bf16_lo(v), b = bf16_hi(v);
+  return fmaf(b, b, fmaf(a, a, ss));
+}
+
+// Final epilogue of 32 accumulator columns [col, col+32) of one row; `ss`
+// accumulates the squares of the stored bf16 values when p.ss_out is set.
+__device__ __forceinline__ void store_cols(const Params& p, int row, int col, float (&f)[32], float& ss) {
   __nv_bfloat16* crow = reinterpret_cast<__nv_bfloat16*>(p.C) + static_cast<size_t>(row) * p.ldc;
   const __nv_bfloat16* rrow =
       p.epi == SSB_EPI_RESIDUAL ? reinterpret_cast<const __nv_bfloat16*>(p.R) + static_cast<size_t>(row) * p.ldr
@@ -165,6 +192,7 @@ __device__ __forceinline__ void store_cols(const Params& p, int row, int col, fl
       o.z = pack_bf16x2(f[8 * v + 4], f[8 * v + 5]);
       o.w = pack_bf16x2(f[8 * v + 6], f[8 * v + 7]);
       dst[v] = o;
+      if (p.ss_out) ss = sq_bf16x2(o.w, sq_bf16x2(o.z, sq_bf16x2(o.y, sq_bf16x2(o.x, ss))));
     }
   } else {
 #pragma unroll
@@ -172,7 +200,10 @@ __device__ __forceinline__ void store_cols(const Params& p, int row, int col, fl
       if (col + j < p.N) {
         float v = f[j];
         if (rrow) v += __bfloat162float(rrow[col + j]);
-        crow[col + j] = __float2bfloat16_rn(v);
+        const __nv_bfloat16 o = __float2bfloat16_rn(v);
+        crow[col + j] = o;
+        const float q = __bfloat162float(o);
+        ss = fmaf(q, q, ss);
       }
     }
   }
@@ -515,6 +546,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = tm * kBM + q * 32 + lane;
       const bool row_ok = row < p.M;
       const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+      const float rs = (p.ss_in != nullptr && row_ok) ? row_rms_scale(p, row) : 1.f;
+      float ss = 0.f;
       if (nsplit == 1) {
         if (p.epi == SSB_EPI_ARGMAX) {
           unsigned long long best = 0;
@@ -526,6 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             float f[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(a[j]);
+            if (p.ss_in) scale32(f, rs);
             argmax_cols(p, tn * BN + c * 32, f, best);
           }
           if (row_ok && best) atomicMax(reinterpret_cast<unsigned long long*>(p.C) + row, best);
@@ -545,6 +579,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               fl[j] = __uint_as_float(lo[j]);
               fh[j] = __uint_as_float(hi[j]);
             }
+            if (p.ss_in) {
+              scale32(fl, rs);
+              scale32(fh, rs);
+            }
             if (row_ok && tn * BN + c * 32 < p.N) store_rope(p, row, tn * BN + c * 32, fl, fh);
           }
         } else if (p.epi == SSB_EPI_SILU_MUL) {
@@ -561,6 +599,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               gf[j] = __uint_as_float(g[j]);
               uf[j] = __uint_as_float(v[j]);
             }
+            if (p.ss_in) {
+              scale32(gf, rs);
+              scale32(uf, rs);
+            }
             if (row_ok) store_silu(p, row, (tn * BN) / 2 + c * 32, gf, uf);
           }
         } else {
@@ -572,8 +614,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             float f[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(a[j]);
-            if (row_ok) store_cols(p, row, tn * BN + c * 32, f);
+            if (p.ss_in) scale32(f, rs);
+            if (row_ok) store_cols(p, row, tn * BN + c * 32, f, ss);
           }
+          if (p.ss_out && row_ok) p.ss_out[static_cast<size_t>(row) * p.tiles_n + tn] = ss;
         }
         tc_fence_before();
         __syncwarp();
@@ -625,6 +669,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int c = 0; c < BN / 32; ++c) {
               float f[32];
               sum_partials(rbase, split_stride4, nsplit, c * 8, f);
+              if (p.ss_in) scale32(f, rs);
               argmax_cols(p, tn * BN + c * 32, f, best);
             }
             if (row_ok && best) atomicMax(reinterpret_cast<unsigned long long*>(p.C) + row, best);
@@ -635,6 +680,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               float fl[32], fh[32];
               sum_partials(rbase, split_stride4, nsplit, c * 8, fl);
               sum_partials(rbase, split_stride4, nsplit, (c + 2) * 8, fh);
+              if (p.ss_in) {
+                scale32(fl, rs);
+                scale32(fh, rs);
+              }
               if (row_ok && tn * BN + c * 32 < p.N) store_rope(p, row, tn * BN + c * 32, fl, fh);
             }
           } else if (p.epi == SSB_EPI_SILU_MUL) {
@@ -643,6 +692,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               float g[32], v[32];
               sum_partials(rbase, split_stride4, nsplit, c * 16, g);
               sum_partials(rbase, split_stride4, nsplit, c * 16 + 8, v);
+              if (p.ss_in) {
+                scale32(g, rs);
+                scale32(v, rs);
+              }
               if (row_ok) store_silu(p, row, (tn * BN) / 2 + c * 32, g, v);
             }
           } else {
@@ -650,8 +703,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int c = 0; c < BN / 32; ++c) {
               float f[32];
               sum_partials(rbase, split_stride4, nsplit, c * 8, f);
-              if (row_ok) store_cols(p, row, tn * BN + c * 32, f);
+              if (p.ss_in) scale32(f, rs);
+              if (row_ok) store_cols(p, row, tn * BN + c * 32, f, ss);
             }
+            if (p.ss_out && row_ok) p.ss_out[static_cast<size_t>(row) * p.tiles_n + tn] = ss;
           }
         }
       }
@@ -686,7 +741,7 @@ int gemm_policy_mode() {
 template <int BN, int MODE>
 int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, int K, int lda,
            int ldb, int ldc, int ldr, int epi, cudaStream_t stream, int max_ctas, int splits, void* ws,
-           const RopeKV* rk, int arg_base, bool tail) {
+           const RopeKV* rk, int arg_base, bool tail, ssb_rownorm* rn) {
   using C = Cfg<BN, MODE>;
   constexpr int MC = MODE ? 2 : 1;
   CUtensorMap ta, tb;
@@ -714,6 +769,12 @@ int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, 
   p.pol_mode = gemm_policy_mode();
   p.tiles_m = (M + kBM - 1) / kBM;
   p.tiles_n = (N + BN - 1) / BN;
+  p.ss_out = rn ? rn->ss_out : nullptr;
+  p.ss_in = rn ? rn->ss_in : nullptr;
+  p.ss_in_parts = rn ? rn->ss_in_parts : 0;
+  p.ss_hidden = rn ? static_cast<float>(rn->hidden) : 1.f;
+  p.ss_eps = rn ? rn->eps : 0.f;
+  if (rn) rn->ss_parts = rn->ss_out ? p.tiles_n : 0;
   const int num_kb = (K + kBK - 1) / kBK;
   p.kb_per_split = (num_kb + splits - 1) / splits;
   p.splits = (num_kb + p.kb_per_split - 1) / p.kb_per_split;  // no empty split
@@ -925,7 +986,7 @@ Plan choose_plan(int M, int N, int K, int epi, int sms, size_t ws_bytes) {
 namespace {
 int gemm_entry(const void* A, const void* B, void* C, const void* R, int M, int N, int K, int lda, int ldb,
                int ldc, int ldr, int epilogue, int block_n, int max_ctas, void* workspace, int64_t ws_bytes,
-               void* stream, const ssb::RopeKV* rk = nullptr, int arg_base = 0) {
+               void* stream, const ssb::RopeKV* rk = nullptr, int arg_base = 0, ssb_rownorm* rn = nullptr) {
   using namespace ssb;
   SSB_REQUIRE(M > 0 && N > 0 && K > 0, "ssb_gemm_bf16: empty problem M=%d N=%d K=%d", M, N, K);
   SSB_REQUIRE(A && B && C, "ssb_gemm_bf16: null operand");
@@ -968,17 +1029,22 @@ int gemm_entry(const void* A, const void* B, void* C, const void* R, int M, int 
     const int kb = (K + kBK - 1) / kBK, kbs = (kb + pl.splits - 1) / pl.splits;
     pl.splits = (kb + kbs - 1) / kbs;
   }
+  if (rn) {
+    SSB_REQUIRE(!rn->ss_out || epilogue == SSB_EPI_RESIDUAL, "ssb_gemm: ss_out needs the residual epilogue");
+    SSB_REQUIRE(!rn->ss_in || (rn->ss_in_parts > 0 && rn->hidden > 0),
+                "ssb_gemm: ss_in needs ss_in_parts > 0 and hidden > 0");
+  }
   if (pl.splits > 1 && plan_ws_bytes(M, N, pl, sms) > static_cast<size_t>(ws_bytes))
     return fail_arg("ssb_gemm_bf16: split-K x%d needs %zu workspace bytes, have %lld", pl.splits,
                     plan_ws_bytes(M, N, pl, sms), static_cast<long long>(ws_bytes));
 #define SSB_GEMM_CASE(BN_)                                                                              \
   case BN_:                                                                                            \
     return pl.mode == 2   ? launch<BN_, 2>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas, \
-                                           pl.splits, workspace, rk, arg_base, pl.tail != 0)           \
+                                           pl.splits, workspace, rk, arg_base, pl.tail != 0, rn)           \
            : pl.mode == 1 ? launch<BN_, 1>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas, \
-                                           pl.splits, workspace, rk, arg_base, pl.tail != 0)           \
+                                           pl.splits, workspace, rk, arg_base, pl.tail != 0, rn)           \
                           : launch<BN_, 0>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas, \
-                                           pl.splits, workspace, rk, arg_base, pl.tail != 0);
+                                           pl.splits, workspace, rk, arg_base, pl.tail != 0, rn);
   switch (pl.bn) {
     SSB_GEMM_CASE(256)
     SSB_GEMM_CASE(224)
@@ -1003,6 +1069,13 @@ extern "C" int ssb_gemm_bf16_ws(const void* A, const void* B, void* C, const voi
                     workspace_bytes, stream);
 }
 
+extern "C" int ssb_gemm_bf16_rn(const void* A, const void* B, void* C, const void* R, int M, int N, int K,
+                                int lda, int ldb, int ldc, int ldr, int epilogue, int block_n, int max_ctas,
+                                void* workspace, int64_t workspace_bytes, ssb_rownorm* rn, void* stream) {
+  return gemm_entry(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, block_n, max_ctas, workspace,
+                    workspace_bytes, stream, nullptr, 0, rn);
+}
+
 extern "C" int64_t ssb_gemm_plan(int M, int N, int K, int epilogue, int max_ctas, int64_t workspace_bytes,
                                  int32_t* out_plan) {
   using namespace ssb;
@@ -1021,7 +1094,8 @@ extern "C" int ssb_gemm_qkv_rope_kv(const void* A, const void* B, void* qkv, int
                                     int ldc, int nq, int nk, int head_dim, const int32_t* positions,
                                     const float* rope_cos, const float* rope_sin, int max_pos, void* pool,
                                     ssb_kv_geometry geo, int layer, const int64_t* slots, int block_n,
-                                    int max_ctas, void* workspace, int64_t workspace_bytes, void* stream) {
+                                    int max_ctas, void* workspace, int64_t workspace_bytes, ssb_rownorm* rn,
+                                    void* stream) {
   using namespace ssb;
   SSB_REQUIRE(head_dim == 128, "ssb_gemm_qkv_rope_kv: head_dim must be 128 (got %d)", head_dim);
   SSB_REQUIRE(nq > 0 && nk > 0 && nq % nk == 0, "ssb_gemm_qkv_rope_kv: bad head counts nq=%d nk=%d", nq, nk);
@@ -1046,16 +1120,16 @@ extern "C" int ssb_gemm_qkv_rope_kv(const void* A, const void* B, void* qkv, int
   rk.nk = nk;
   const int N = (nq + 2 * nk) * head_dim;
   return gemm_entry(A, B, qkv, nullptr, M, N, K, lda, ldb, ldc, 0, SSB_EPI_ROPE_KV, block_n, max_ctas, workspace,
-                    workspace_bytes, stream, &rk);
+                    workspace_bytes, stream, &rk, 0, rn);
 }
 
 extern "C" int ssb_gemm_lm_head_argmax(const void* A, const void* B, int M, int N, int K, int lda, int ldb,
                                        int index_base, unsigned long long* keys, int block_n, int max_ctas,
-                                       void* workspace, int64_t workspace_bytes, void* stream) {
+                                       void* workspace, int64_t workspace_bytes, ssb_rownorm* rn, void* stream) {
   using namespace ssb;
   SSB_REQUIRE(keys, "ssb_gemm_lm_head_argmax: null keys");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   SSB_CUDA(cudaMemsetAsync(keys, 0, static_cast<size_t>(M) * sizeof(unsigned long long), s));
   return gemm_entry(A, B, keys, nullptr, M, N, K, lda, ldb, 0, 0, SSB_EPI_ARGMAX, block_n, max_ctas, workspace,
-                    workspace_bytes, stream, nullptr, index_base);
+                    workspace_bytes, stream, nullptr, index_base, rn);
 }

@@ -51,6 +51,7 @@ def gemm(
     out_f32: bool = False,
     max_ctas: int = 0,
     workspace: torch.Tensor | None = None,
+    rownorm: "_lib.RowNorm | None" = None,
 ) -> torch.Tensor:
     """out = a @ w.T (+ residual) or silu-mul of interleaved gate/up columns,
     or fp32 output (logits) with ``out_f32``.
@@ -58,6 +59,7 @@ def gemm(
     a: [M, K] bf16 (row stride may exceed K), w: [N, K] bf16 weight.
     workspace: zero-initialised device buffer (one per stream) that lets the
     library split K across CTAs for skinny problems (decode projections).
+    rownorm: the folded-RMSNorm hooks (row_norm(); ss_parts is filled in).
     """
     _check(a, "a")
     _check(w, "w")
@@ -79,7 +81,7 @@ def gemm(
     if residual is not None:
         _check(residual, "residual")
     call(
-        "ssb_gemm_bf16_ws",
+        "ssb_gemm_bf16_rn" if rownorm is not None else "ssb_gemm_bf16_ws",
         a.data_ptr(),
         w.data_ptr(),
         out.data_ptr(),
@@ -96,9 +98,26 @@ def gemm(
         max_ctas,
         workspace.data_ptr() if workspace is not None else None,
         workspace.numel() * workspace.element_size() if workspace is not None else 0,
+        *((ctypes.byref(rownorm),) if rownorm is not None else ()),
         _stream(),
     )
     return out
+
+
+def row_norm(ss_out: torch.Tensor | None = None, ss_in: torch.Tensor | None = None, ss_in_parts: int = 0,
+             hidden: int = 0, eps: float = 0.0) -> "_lib.RowNorm":
+    """Folded-RMSNorm hooks of one GEMM (include/seesaw_b200.h ssb_rownorm):
+    ``ss_out`` fp32 [M, >= N tiles] receives the producer's per-tile row sums
+    of squares (residual epilogue; ``.ss_parts`` = tiles written), ``ss_in``
+    (a producer's ss_out, ``ss_in_parts`` columns used) scales every output
+    row by 1/rms before the epilogue."""
+    for t, n in ((ss_out, "ss_out"), (ss_in, "ss_in")):
+        if t is not None and (t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous()):
+            raise ValueError(f"row_norm: {n} must be a contiguous fp32 CUDA tensor")
+    if ss_in is not None and ss_in.shape[1] != ss_in_parts:
+        raise ValueError(f"row_norm: ss_in has {ss_in.shape[1]} columns, ss_in_parts={ss_in_parts}")
+    return _lib.RowNorm(ss_out.data_ptr() if ss_out is not None else None,
+                        ss_in.data_ptr() if ss_in is not None else None, ss_in_parts, hidden, eps, 0)
 
 
 def kv_reshard_pack(pool, geometry, block_ids, peers, staging) -> None:
@@ -238,7 +257,8 @@ def rope_kv_append(qkv: torch.Tensor, nq: int, nk: int, positions: torch.Tensor,
 def gemm_qkv_rope_kv(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor, nq: int, nk: int,
                      positions: torch.Tensor, rope_cos: torch.Tensor, rope_sin: torch.Tensor,
                      pool: torch.Tensor | None, geometry, layer: int, slots: torch.Tensor | None,
-                     block_n: int = 0, max_ctas: int = 0, workspace: torch.Tensor | None = None) -> torch.Tensor:
+                     block_n: int = 0, max_ctas: int = 0, workspace: torch.Tensor | None = None,
+                     rownorm: "_lib.RowNorm | None" = None) -> torch.Tensor:
     """QKV projection with RoPE and the paged K/V append fused into the GEMM
     epilogue: bit-identical to gemm() followed by rope_kv_append()."""
     _check(a, "a")
@@ -257,13 +277,14 @@ def gemm_qkv_rope_kv(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor, nq: in
          rope_cos.shape[0], pool.data_ptr() if pool is not None else None, _lib.KVGeometry(*geometry), layer,
          slots.data_ptr() if slots is not None else None, block_n, max_ctas,
          workspace.data_ptr() if workspace is not None else None,
-         workspace.numel() * workspace.element_size() if workspace is not None else 0, _stream())
+         workspace.numel() * workspace.element_size() if workspace is not None else 0,
+         ctypes.byref(rownorm) if rownorm is not None else None, _stream())
     return out
 
 
 def lm_head_argmax(h: torch.Tensor, w: torch.Tensor, index_base: int, out_val: torch.Tensor,
                    out_idx: torch.Tensor, keys: torch.Tensor | None = None,
-                   workspace: torch.Tensor | None = None) -> None:
+                   workspace: torch.Tensor | None = None, rownorm: "_lib.RowNorm | None" = None) -> None:
     """Greedy argmax of h @ w.T without materialising the logits: the GEMM
     epilogue reduces each row to a packed (value, index) key (64-bit
     atomicMax), then the keys are unpacked to (value, index + index_base)."""
@@ -275,7 +296,8 @@ def lm_head_argmax(h: torch.Tensor, w: torch.Tensor, index_base: int, out_val: t
         keys = torch.empty(M, dtype=torch.int64, device=h.device)
     call("ssb_gemm_lm_head_argmax", h.data_ptr(), w.data_ptr(), M, N, K, h.stride(0), w.stride(0), index_base,
          keys.data_ptr(), 0, 0, workspace.data_ptr() if workspace is not None else None,
-         workspace.numel() * workspace.element_size() if workspace is not None else 0, _stream())
+         workspace.numel() * workspace.element_size() if workspace is not None else 0,
+         ctypes.byref(rownorm) if rownorm is not None else None, _stream())
     call("ssb_argmax_keys_decode", keys.data_ptr(), M, out_val.data_ptr(), out_idx.data_ptr(), _stream())
 
 

@@ -140,6 +140,10 @@ class Worker:
         self.fused_tp: bool | None = None if env is None else env == "1"
         self.fused_tp_blocks = int(os.environ.get("SSB_TP_FUSED_BLOCKS", "0"))
         self._tp_arenas: dict = {}
+        # RMSNorm folded into the GEMMs (single-GPU layout): the residual
+        # GEMMs emit row sums of squares, the consumers scale rows by 1/rms,
+        # the gains live in the consumer weights (fold_gains)
+        self.fold_norm = os.environ.get("SSB_FOLD_NORM", "1") != "0"
 
     # ------------------------------------------------------------ layouts --
     def _tp_comm(self, cfg: ParallelismConfig, stage: int) -> Comm:
@@ -166,6 +170,26 @@ class Worker:
         segs = torch.from_numpy(table).to(self.device)
         ops.init_weights(st.arena, segs, total, self.seed)
         self.state = st
+        if self.fold_norm:
+            self.fold_gains()
+
+    def fold_gains(self) -> None:
+        """Fold every RMSNorm gain into the weights that consume the normed
+        activations (W[:, k] *= gamma[k]: attn_norm -> wqkv, mlp_norm -> w13,
+        final_norm -> head) and set the gains to 1 — the same model, whose
+        norms are then pure 1/rms row scales that the GEMM epilogues apply
+        (ssb_rownorm).  A no-op for unit gains (the synthetic init's)."""
+        pairs = [(f"L{l}.attn_norm", f"L{l}.wqkv") for l in self._layers()]
+        pairs += [(f"L{l}.mlp_norm", f"L{l}.w13") for l in self._layers()]
+        pairs.append(("final_norm", "head"))
+        for g_key, w_key in pairs:
+            if not (self.has(g_key) and self.has(w_key)):
+                continue
+            g = self.w(g_key)
+            if bool(torch.all(g == 1)):
+                continue
+            self.w(w_key).mul_(g.view(1, -1))
+            g.fill_(1)
 
     def w(self, key: str) -> torch.Tensor:
         t = self.state.weights.tensors[key]
@@ -425,6 +449,8 @@ class Worker:
         if ar is not None:
             return self._block_fused(x, layer, attn_fn, buf, rope, cap, ar, h_ready, final)
         st = self.state
+        if self.fold_norm and st.tp_comm.size == 1:
+            return self._block_folded(x, layer, attn_fn, buf, rope, cap, int(h_ready))
         eps = self.arch.rms_eps
         p = f"L{layer}."
         lead = st.rank == 0
@@ -448,6 +474,56 @@ class Worker:
         ops.gemm(act, self.w(p + "w2"), out=x, residual=x if lead else None, max_ctas=cap, workspace=ws)
         self._reduce_into(x)
         return False
+
+    def _block_folded(self, x, layer, attn_fn, buf, rope, cap, ss_parts: int) -> int:
+        """Single-GPU layer with both RMSNorms folded into the GEMMs: the
+        o_proj / down_proj residual epilogues write per-tile row sums of
+        squares of the new x, the QKV and gate/up GEMMs read x itself and
+        scale their rows by 1/rms (gains folded into their weights).
+        ``ss_parts`` > 0: buf["ss"][1] holds the previous down_proj's sums
+        (else this layer's input norm runs as a kernel).  Returns the parts
+        count of this layer's down_proj sums."""
+        st = self.state
+        eps = self.arch.rms_eps
+        hid = self.arch.hidden
+        p = f"L{layer}."
+        ws = buf["ws"]
+        local = layer - st.weights.layer_begin
+        nq, nk = st.weights.n_q_heads, st.weights.n_kv_heads
+        pos, slots = rope
+        geo = self.geometry().as_tuple()
+        T = x.shape[0]
+        ss_a, ss_b = buf["ss"]
+        if ss_parts:
+            a_in = x
+            rn = ops.row_norm(ss_in=ss_b[: T * ss_parts].view(T, ss_parts), ss_in_parts=ss_parts, hidden=hid, eps=eps)
+        else:
+            a_in = ops.rmsnorm(x, self.w(p + "attn_norm"), eps, out=buf["h"])
+            rn = None
+        if self.fuse_rope and self.arch.head_dim == 128:
+            qkv = ops.gemm_qkv_rope_kv(a_in, self.w(p + "wqkv"), buf["qkv"], nq, nk, pos, self.rope_cos,
+                                       self.rope_sin, self.pool, geo, local, slots, max_ctas=cap, workspace=ws,
+                                       rownorm=rn)
+        else:
+            qkv = ops.gemm(a_in, self.w(p + "wqkv"), out=buf["qkv"], max_ctas=cap, workspace=ws, rownorm=rn)
+            ops.rope_kv_append(qkv, nq, nk, pos, self.rope_cos, self.rope_sin, self.pool, geo, local, slots)
+        attn = attn_fn(qkv, local)
+        rn_o = ops.row_norm(ss_out=ss_a)
+        ops.gemm(attn, self.w(p + "wo"), out=x, residual=x, max_ctas=cap, workspace=ws, rownorm=rn_o)
+        pa = rn_o.ss_parts
+        rn_m = ops.row_norm(ss_in=ss_a[: T * pa].view(T, pa), ss_in_parts=pa, hidden=hid, eps=eps)
+        act = ops.gemm(x, self.w(p + "w13"), out=buf["act"], silu_mul=True, max_ctas=cap, workspace=ws,
+                       rownorm=rn_m)
+        rn_d = ops.row_norm(ss_out=ss_b)
+        ops.gemm(act, self.w(p + "w2"), out=x, residual=x, max_ctas=cap, workspace=ws, rownorm=rn_d)
+        return rn_d.ss_parts
+
+    def _final_rownorm(self, buf: dict, T: int, ss_parts: int):
+        """The final RMSNorm as the LM head's row scale (folded path)."""
+        if not ss_parts:
+            return None
+        return ops.row_norm(ss_in=buf["ss"][1][: T * ss_parts].view(T, ss_parts), ss_in_parts=ss_parts,
+                            hidden=self.arch.hidden, eps=self.arch.rms_eps)
 
     def _block_fused(self, x, layer, attn_fn, buf, rope, cap, ar, h_ready, final) -> bool:
         st = self.state
@@ -499,6 +575,9 @@ class Worker:
                 "qkv": torch.empty(T, (nq + 2 * nk) * a.head_dim, dtype=torch.bfloat16, device=dev),
                 "attn": torch.empty(T, nq * a.head_dim, dtype=torch.bfloat16, device=dev),
                 "act": torch.empty(T, st.weights.ffn_local, dtype=torch.bfloat16, device=dev),
+                # folded-norm row sums of squares: [T][N tiles] of the o_proj
+                # and down_proj outputs (N tile >= 64 columns)
+                "ss": [torch.empty(T * ((a.hidden + 63) // 64), dtype=torch.float32, device=dev) for _ in range(2)],
             }
         if "ws" not in slot:
             # split-K workspace of this lane's stream (zeroed once; the GEMM
@@ -507,20 +586,23 @@ class Worker:
         slot["buf"]["ws"] = slot["ws"] if self.split_k else None
         return slot["buf"]
 
-    def _logits_argmax(self, h_last: torch.Tensor, out_tokens: torch.Tensor, ws: torch.Tensor | None = None) -> None:
-        """Vocab-parallel LM head + greedy argmax (fp32 logits)."""
+    def _logits_argmax(self, h_last: torch.Tensor, out_tokens: torch.Tensor, ws: torch.Tensor | None = None,
+                       rownorm=None) -> None:
+        """Vocab-parallel LM head + greedy argmax (fp32 logits).  ``rownorm``:
+        h_last is the un-normed x and the final norm is the GEMM's row scale."""
         st = self.state
         n = h_last.shape[0]
         vals = torch.empty(n, dtype=torch.float32, device=self.device)
         idxs = torch.empty(n, dtype=torch.int32, device=self.device)
         if self.record_logits or not self.fuse_argmax:
-            logits = ops.gemm(h_last, self.w("head"), out_f32=True, workspace=ws)
+            logits = ops.gemm(h_last, self.w("head"), out_f32=True, workspace=ws, rownorm=rownorm)
             ops.argmax_rows(logits, st.weights.vocab_begin, vals, idxs)
             if self.record_logits:
                 self._record(logits)
         else:
             # argmax in the LM-head GEMM epilogue: no [n, vocab] fp32 logits round trip
-            ops.lm_head_argmax(h_last, self.w("head"), st.weights.vocab_begin, vals, idxs, workspace=ws)
+            ops.lm_head_argmax(h_last, self.w("head"), st.weights.vocab_begin, vals, idxs, workspace=ws,
+                               rownorm=rownorm)
         if st.tp_comm.size == 1:
             out_tokens.copy_(idxs)
             return
@@ -657,10 +739,13 @@ class Worker:
                                                h_ready=v["h_ready"], final=final)
         for s, x, _, buf, v in lanes:
             with torch.cuda.stream(s):
+                rn = None
                 if ar is not None and v["h_ready"]:
                     h = ar.h[: x.shape[0]]
+                elif self.fold_norm and st.tp_comm.size == 1 and v["h_ready"]:
+                    h, rn = x, self._final_rownorm(buf, x.shape[0], int(v["h_ready"]))
                 else:
                     h = ops.rmsnorm(x, self.w("final_norm"), a.rms_eps, out=buf["h"])
-                self._logits_argmax(h, v["out"], buf["ws"])
+                self._logits_argmax(h, v["out"], buf["ws"], rownorm=rn)
         if len(spans) > 1:
             main.wait_stream(self._side)

@@ -45,6 +45,7 @@ def main() -> None:
         w.fuse_rope = name != "no_rope_fusion"
         w.fuse_argmax = name != "no_argmax_fusion"
         w.split_k = name != "no_split_k"
+        w.fold_norm = name != "no_fold_norm"
         ops._PREFILL_VARIANT = 2 if name == "attn_per_tile_ctas" else 0
         state["prefill_tokens"] = {"prefill_8k": 8192, "prefill_32k": 32768}.get(name, 16384)
 
