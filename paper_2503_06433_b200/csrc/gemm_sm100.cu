@@ -138,8 +138,25 @@ __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x));
 // rmsnorm kernel's formula (parts summed in order: deterministic).
 __device__ __forceinline__ float row_rms_scale(const Params& p, int row) {
   const float* src = p.ss_in + static_cast<size_t>(row) * p.ss_in_parts;
+  const int n = p.ss_in_parts;
   float ss = 0.f;
-  for (int j = 0; j < p.ss_in_parts; ++j) ss += src[j];
+  int j = 0;
+  if ((n & 3) == 0) {  // 16-byte rows: 8 independent vector loads in flight
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    for (; j + 32 <= n; j += 32) {
+      float4 v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = s4[j / 4 + i];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ss = ss + v[i].x + v[i].y + v[i].z + v[i].w;
+    }
+    for (; j < n; j += 4) {
+      const float4 v = s4[j / 4];
+      ss = ss + v.x + v.y + v.z + v.w;
+    }
+  } else {
+    for (; j < n; ++j) ss += src[j];
+  }
   return 1.0f / sqrtf(__fadd_rn(__fdiv_rn(ss, p.ss_hidden), p.ss_eps));
 }
 
@@ -541,12 +558,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       unit_decode(p, u, t, split, nsplit);
       tile_coords(t, units_m, p.tiles_n, p.group_n, p.group_size, um, tn);
       const int tm = um * MC + crank;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
       const int row = tm * kBM + q * 32 + lane;
       const bool row_ok = row < p.M;
-      const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+      // the row's 1/rms: loads issued while the tile's MMAs still run
       const float rs = (p.ss_in != nullptr && row_ok) ? row_rms_scale(p, row) : 1.f;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       float ss = 0.f;
       if (nsplit == 1) {
         if (p.epi == SSB_EPI_ARGMAX) {

@@ -79,6 +79,11 @@ def test_consumer_row_scale(cuda, M, N, K):
     torch.cuda.synchronize()
     assert (y.float() - ref).abs().max().item() < tol
     assert (f - ref).abs().max().item() < 1e-3 * ref.abs().max().item()
+    for odd in (7, 37):  # parts not a multiple of 4: the scalar load path
+        rn_odd = ops.row_norm(ss_in=_split_ss(x, odd), ss_in_parts=odd, hidden=K, eps=EPS)
+        f_odd = ops.gemm(x, w, out_f32=True, workspace=ws, rownorm=rn_odd)
+        torch.cuda.synchronize()
+        assert (f_odd - ref).abs().max().item() < 1e-3 * ref.abs().max().item()
     # SiLU(gate) * up on the scaled rows
     if N % 64 == 0:
         F = N // 2
