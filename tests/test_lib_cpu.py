@@ -51,3 +51,30 @@ def test_argument_errors_are_reported_not_raised():
         p32 = ctypes.cast(arr, ctypes.POINTER(ctypes.c_int32))
         p64 = ctypes.cast(_lib.int64_array([0]), ctypes.POINTER(ctypes.c_int64))
         _lib.call("ssb_kv_reshard_pack", None, geo, None, 1, 0, p32, p32, p32, p32, p64, None, None)
+
+
+def test_struct_layouts_match_header():
+    """ctypes mirrors of the header's structs: sizes and field offsets as a
+    C compiler lays them out (x86-64 / aarch64 LP64)."""
+    import ctypes
+
+    assert ctypes.sizeof(_lib.RowNorm) == 32
+    assert _lib.RowNorm.ss_in.offset == 8 and _lib.RowNorm.ss_in_parts.offset == 16
+    assert _lib.RowNorm.eps.offset == 24 and _lib.RowNorm.ss_parts.offset == 28
+    assert ctypes.sizeof(_lib.CopyDesc) == 48
+
+
+def test_rownorm_and_tp_combine_argument_errors():
+    lib = _lib.load()
+    rn = _lib.RowNorm(None, 1, 0, 0, 0.0, 0)  # ss_in without parts
+    import ctypes
+
+    rc = lib.ssb_gemm_bf16_rn(16, 16, 16, None, 128, 128, 64, 64, 64, 128, 0, 0, 0, 0, None, 0, ctypes.byref(rn),
+                              None)
+    assert rc < 0 and b"ss_in" in lib.ssb_last_error()
+    assert lib.ssb_tp_signal_bytes() == 2 * 512 * 8 * 4
+    addrs = _lib.uint64_array([16, 32])
+    rc = lib.ssb_tp_allreduce_rmsnorm(addrs, addrs, None, addrs, 2, 0, 4, 256, 256, None, 1e-5, 0, 4, None, None)
+    assert rc < 0 and b"epoch" in lib.ssb_last_error()
+    rc = lib.ssb_tp_allreduce_rmsnorm(addrs, addrs, None, addrs, 9, 0, 4, 256, 256, None, 1e-5, 1, 4, None, None)
+    assert rc < 0 and b"nranks" in lib.ssb_last_error()
