@@ -97,6 +97,10 @@ struct Params {
   const float* ss_in;
   int ss_in_parts;
   float ss_hidden, ss_eps;
+  // serpentine K: a CTA's odd-numbered units walk their k-blocks backwards,
+  // so a wave starts on the operand slabs the previous wave touched last
+  // (still in L2) instead of the ones it evicted first
+  int kserp;
 };
 
 // Grouped rasterisation: kGroupM tiles of the "band" dimension share one
@@ -465,7 +469,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int tm = um * MC + crank;
         const int kb0 = nsplit > 1 ? split * p.kb_per_split : 0;
         const int kb1 = nsplit > 1 ? min(num_kb, kb0 + p.kb_per_split) : num_kb;
-        for (int kb = kb0; kb < kb1; ++kb) {
+        const bool rev = p.kserp && (((u - cid) / nclusters) & 1);
+        for (int i = kb0; i < kb1; ++i) {
+          // (the MMA warp only counts k-blocks: the order is the producer's)
+          const int kb = rev ? kb1 - 1 - (i - kb0) : i;
           mbar_wait(&empty[stage], phase ^ 1);
           if (MODE == 2) {
             // both halves land on the leader's full barrier
@@ -785,6 +792,10 @@ int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, 
   if (rk) p.rk = *rk;
   p.arg_base = arg_base;
   p.pol_mode = gemm_policy_mode();
+  {
+    static const int kserp = gemm_env("SSB_GEMM_KSERP", 1);
+    p.kserp = kserp;
+  }
   p.tiles_m = (M + kBM - 1) / kBM;
   p.tiles_n = (N + BN - 1) / BN;
   p.ss_out = rn ? rn->ss_out : nullptr;
