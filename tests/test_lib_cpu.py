@@ -78,3 +78,28 @@ def test_rownorm_and_tp_combine_argument_errors():
     assert rc < 0 and b"epoch" in lib.ssb_last_error()
     rc = lib.ssb_tp_allreduce_rmsnorm(addrs, addrs, None, addrs, 9, 0, 4, 256, 256, None, 1e-5, 1, 4, None, None)
     assert rc < 0 and b"nranks" in lib.ssb_last_error()
+
+
+def test_tp_arena_cache_grows_collectively(monkeypatch):
+    """tpcombine.get_arena: one arena per (TP group, hidden), rebuilt only to
+    grow (power-of-two rows, never below 256), and an arena whose self-test
+    failed is remembered as unusable (every later call falls back)."""
+    from paper_2503_06433_b200 import tpcombine
+
+    built = []
+
+    class FakeArena:
+        def __init__(self, comm, device, hidden, rows, max_blocks):
+            self.rows, self.usable = rows, comm != "bad"
+            built.append(rows)
+
+    monkeypatch.setattr(tpcombine, "PeerArena", FakeArena)
+    cache: dict = {}
+    a = tpcombine.get_arena(cache, "grp", None, 4096, 100, 16)
+    assert a.rows == 256 and built == [256]
+    assert tpcombine.get_arena(cache, "grp", None, 4096, 256, 16) is a
+    b = tpcombine.get_arena(cache, "grp", None, 4096, 300, 16)
+    assert b.rows == 512 and built == [256, 512]
+    assert tpcombine.get_arena(cache, "grp", None, 4096, 17, 16) is b
+    assert tpcombine.get_arena(cache, "bad", None, 4096, 10, 16) is None
+    assert tpcombine.get_arena(cache, "bad", None, 4096, 10, 16) is None and built == [256, 512, 256]
