@@ -26,7 +26,7 @@ import torch.multiprocessing as mp
 pytestmark = pytest.mark.gpu
 
 
-def _rank(rank: int, port: int, outdir: str, tiered: bool, p2p: bool = False) -> None:
+def _rank(rank: int, port: int, outdir: str, tiered: bool, p2p: bool = False, fused_tp: bool = False) -> None:
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -58,6 +58,7 @@ def _rank(rank: int, port: int, outdir: str, tiered: bool, p2p: bool = False) ->
     comm = TorchComm()
     wk = Worker(arch, comm, 1, dev, seed=0, max_pos=256)
     wk.p2p_reshard = p2p
+    wk.fused_tp = fused_tp
     rep = execute(model, hw, reqs, SchedulingPolicy.TRANSITION_MINIMIZING, ParallelismConfig(1, 2, 1),
                   ParallelismConfig(2, 1, 1), arch=arch, prompts=prompts, comm=comm, device=dev, worker=wk)
     torch.cuda.synchronize()
@@ -67,7 +68,8 @@ def _rank(rank: int, port: int, outdir: str, tiered: bool, p2p: bool = False) ->
     with open(f"{outdir}/rank{rank}.pkl", "wb") as fh:
         pickle.dump({"outputs": rep.outputs, "replay": bool(replay_check(rep)), "kinds": kinds,
                      "transitions": rep.transitions, "host_tier": rep.config["host_tier"],
-                     "sent": rep.measured["reshard_bytes_sent"]}, fh)
+                     "sent": rep.measured["reshard_bytes_sent"],
+                     "fused": bool(wk._tp_arenas) and all(a.usable for a in wk._tp_arenas.values())}, fh)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -78,22 +80,28 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("tiered,p2p", [(False, False), (True, False), (False, True)])
-def test_two_process_pp2_tp2(cuda, tiered, p2p):
+@pytest.mark.parametrize("tiered,p2p,fused_tp", [(False, False, False), (True, False, False), (False, True, False),
+                                                (False, False, True)])
+def test_two_process_pp2_tp2(cuda, tiered, p2p, fused_tp):
     """(p2p: the KV re-shard's pack kernel stores straight into the other
-    process's receive buffer through a CUDA IPC mapping.)"""
+    process's receive buffer through a CUDA IPC mapping.  fused_tp: the TP
+    decode combine is the peer-memory kernel with its device-side barrier,
+    across two processes — their contexts time-slice the one GPU, so every
+    barrier waits for a context switch: slow, but it exercises the
+    cross-process IPC mappings and flag ordering.)"""
     from paper_2503_06433_b200 import PRESETS
     from paper_2503_06433_b200.engine import synthetic_prompts
     from paper_2503_06433_b200.specs import Request
     from test_engine_gpu import check_greedy
 
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_rank, args=(_free_port(), d, tiered, p2p), nprocs=2, join=True)
+        mp.spawn(_rank, args=(_free_port(), d, tiered, p2p, fused_tp), nprocs=2, join=True)
         res = [pickle.load(open(f"{d}/rank{r}.pkl", "rb")) for r in range(2)]
     for r in res:
         assert r["replay"] and r["transitions"] == 1 and r["host_tier"] == tiered
         assert r["kinds"]["prefill_complete"] == 8 and r["kinds"]["kv_release"] == 8
         assert r["sent"] > 0
+        assert r["fused"] == fused_tp
     if tiered:
         assert res[0]["kinds"]["swap_in_complete"] == res[0]["kinds"]["swap_out_complete"] >= 1
     # both ranks of the replica produce the same tokens; they match the oracle
