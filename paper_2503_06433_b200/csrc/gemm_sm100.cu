@@ -723,6 +723,37 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
               if (row_ok) store_silu(p, row, (tn * BN) / 2 + c * 32, g, v);
             }
+          } else if (nsplit == 2) {
+            // software-pipelined: the next chunk's two partials are in flight
+            // while this chunk is converted and stored (otherwise every chunk
+            // costs a full L2 round trip after the previous chunk's stores)
+            float4 x0[8], x1[8];
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              x0[v] = __ldcg(rbase + v * kBM);
+              x1[v] = __ldcg(rbase + split_stride4 + v * kBM);
+            }
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+              float f[32];
+#pragma unroll
+              for (int v = 0; v < 8; ++v) {
+                f[4 * v] = x0[v].x + x1[v].x;
+                f[4 * v + 1] = x0[v].y + x1[v].y;
+                f[4 * v + 2] = x0[v].z + x1[v].z;
+                f[4 * v + 3] = x0[v].w + x1[v].w;
+              }
+              if (c + 1 < BN / 32) {
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                  x0[v] = __ldcg(rbase + ((c + 1) * 8 + v) * kBM);
+                  x1[v] = __ldcg(rbase + split_stride4 + ((c + 1) * 8 + v) * kBM);
+                }
+              }
+              if (p.ss_in) scale32(f, rs);
+              if (row_ok) store_cols(p, row, tn * BN + c * 32, f, ss);
+            }
+            if (p.ss_out && row_ok) p.ss_out[static_cast<size_t>(row) * p.tiles_n + tn] = ss;
           } else {
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
