@@ -40,6 +40,19 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 WORKLOAD = {"arch": "llama3-8b", "prompts": 512, "input_len": 1024, "output_len": 256}
+METRIC = "offline output tokens/sec (whole box), PP-prefill -> re-shard -> TP-decode"
+
+
+def _config(args, n: int) -> dict:
+    """The workload named in both arms' lines (BASELINE.json configs[1])."""
+    return {
+        "workload": f"{Path(args.arch).stem} {args.prompts} prompts x {args.input_len} in / {args.output_len} out, "
+                    f"prefill tp1.pp{n} -> decode tp{n}.pp1 (BASELINE.json configs[1] shape)",
+        "prompts": args.prompts, "input_len": args.input_len, "output_len": args.output_len,
+        "parallelism": f"pp{n}->tp{n}", "l2": "inputs >> L2 (weights+KV ~102 GB at N=1); no flush",
+        "policy": "transition-min (b200-native: KV kept in HBM, re-sharded over NVLink)",
+        "prefill_tokens_per_forward": args.prefill_tokens if n == 1 else "1 prompt per micro-batch",
+    }
 
 
 def _peaks() -> dict:
@@ -101,6 +114,17 @@ class ClockSampler:
                 "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
 
 
+def _arch(name: str):
+    """A preset name (PRESETS) or the path of a LlamaArch YAML document."""
+    from paper_2503_06433_b200 import PRESETS, load_arch
+
+    if name in PRESETS:
+        return PRESETS[name]
+    if Path(name).is_file():
+        return load_arch(name)
+    raise SystemExit(f"--arch {name!r}: not a preset ({', '.join(PRESETS)}) nor a LlamaArch YAML file")
+
+
 # ------------------------------------------------------------------ ours --
 def run_ours(args) -> None:
     import torch
@@ -136,7 +160,7 @@ def run_ours(args) -> None:
         comm = TorchComm()
     else:
         comm = SoloComm()
-    arch = PRESETS[args.arch]
+    arch = _arch(args.arch)
     model = arch.model_spec()
     props = torch.cuda.get_device_properties(dev)
     peaks = _peaks()
@@ -223,7 +247,7 @@ def run_ours(args) -> None:
     da = kern.get("decode_attention", {})
     reshard_s = rep.reshard_time
     line = {
-        "metric": "offline output tokens/sec (whole box), PP-prefill -> re-shard -> TP-decode",
+        "metric": METRIC,
         "value": value,
         "unit": "tokens/s",
         "n_gpus": n,
@@ -235,15 +259,7 @@ def run_ours(args) -> None:
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (random-init weights, uniform prompt ids seed 1)",
-        "config": {
-            "workload": f"{args.arch} {args.prompts} prompts x {args.input_len} in / {args.output_len} out, "
-                        f"prefill tp1.pp{n} -> decode tp{n}.pp1 (BASELINE.json configs[1] shape)",
-            "prompts": args.prompts, "input_len": args.input_len, "output_len": args.output_len,
-            "parallelism": f"pp{n}->tp{n}", "l2": "inputs >> L2 (weights+KV ~102 GB at N=1); no flush",
-            "policy": "transition-min (b200-native: KV kept in HBM, re-sharded over NVLink)",
-            "prefill_tokens_per_forward": args.prefill_tokens if n == 1 else "1 prompt per micro-batch",
-            "gpu": props.name,
-        },
+        "config": dict(_config(args, n), gpu=props.name),
         "e2e": {"value": out_tokens / e2e_t, "unit": "tokens/s",
                 "h2d_bytes_per_step": int(sum(p.numel() * 4 for p in prompts_pinned)),
                 "d2h_bytes_per_step": int(args.prompts * (args.output_len + 1) * 4)},
@@ -264,7 +280,7 @@ def run_ours(args) -> None:
     if n == 1:
         line["reshard_micro"] = reshard_microbench(worker, arch, args, peaks)
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args, arch, sample_in=args.cpu_sample_in)
+        line["cpu_baseline"] = cpu_baseline(args, arch)
     print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -479,127 +495,177 @@ def profile_kernels(one, prompts, arch, args, dev, comm, world) -> dict:
 
 
 # ------------------------------------------------------- CPU baseline --
-_CPU_WEIGHTS: dict = {}
+_SLICE_WEIGHTS: dict = {}
 
 
-def cpu_baseline(args, arch, sample_in: int = 256, batch: int = 8) -> dict:
-    """The CPU restatement (oracle/llama.py, fp32 torch, all host threads) on
-    a bounded sample of the workload: one prompt of ``sample_in`` tokens
-    through the full model (prefill cost per token), then one decode step of
-    ``batch`` new tokens (the GEMM shapes of a batch-``batch`` decode step).
-    Extrapolated to the whole batch: T = P*S_in*t_tok + S_out*(P/batch)*t_step,
-    value = P*S_out / T (GEMM-dominated, linear in tokens)."""
+def _slice_weights(arch) -> dict:
+    """fp32 weights of ONE layer + final norm + LM head at ``arch``'s shape,
+    seeded Gaussians at the init's scales (oracle/llama.py tensor_specs).
+    The CPU sample's time depends on the shapes only; drawing them with
+    torch on the host keeps the CPU arm free of the GPU and of this repo's
+    library (the counter-based init in numpy would take ~90 s for these
+    750 M elements)."""
+    import torch
+
+    from oracle import llama as lo
+
+    key = (arch.hidden, arch.num_query_heads, arch.num_kv_heads, arch.head_dim, arch.ffn, arch.vocab)
+    if key not in _SLICE_WEIGHTS:
+        a1 = lo.Arch(1, arch.hidden, arch.num_query_heads, arch.num_kv_heads, arch.head_dim, arch.ffn, arch.vocab,
+                     arch.rope_theta, arch.rms_eps)
+        g = torch.Generator().manual_seed(0)
+        w = {}
+        for name, (_, rows, cols, scale) in lo.tensor_specs(a1).items():
+            if name == "embed":
+                continue  # the sample starts from hidden states: an embedding lookup is a gather
+            w[name] = torch.ones(rows, cols) if scale == 0.0 else torch.randn(rows, cols, generator=g) * scale
+        _SLICE_WEIGHTS.clear()
+        _SLICE_WEIGHTS[key] = (a1, w)
+    return _SLICE_WEIGHTS[key]
+
+
+def cpu_port_sample(arch, s_in: int, ctx: int, batch: int = 8) -> dict:
+    """One bounded sample of the CPU port of the path (oracle/llama.py, fp32
+    torch on every host thread; no GPU, no repo library):
+
+    * prefill: one prompt of ``s_in`` tokens through one full layer (causal
+      attention), then the final norm + LM head of its last token;
+    * decode: one decode step of ``batch`` independent sequences at context
+      ``ctx`` through one full layer (batched projections and MLP, each
+      sequence's attention over its own cache: LlamaOracle.layer_decode_batch),
+      then the final norm + LM head of the ``batch`` rows."""
     import torch
 
     from oracle import llama as lo
 
     threads = os.cpu_count() or 1
     torch.set_num_threads(threads)
-    oa = lo.Arch(arch.num_layers, arch.hidden, arch.num_query_heads, arch.num_kv_heads, arch.head_dim, arch.ffn,
-                 arch.vocab, arch.rope_theta, arch.rms_eps)
-    if arch.name not in _CPU_WEIGHTS:
-        _CPU_WEIGHTS[arch.name] = _cpu_weights(arch)
-    orc = lo.LlamaOracle(oa, seed=0, bf16_faithful=False, max_pos=sample_in + batch + 8,
-                         weights=_CPU_WEIGHTS[arch.name])
-    prompt = np.random.default_rng(1).integers(0, arch.vocab, size=sample_in).astype(np.int64)
-    cache: dict = {}
+    a1, w = _slice_weights(arch)
+    orc = lo.LlamaOracle(a1, seed=0, bf16_faithful=False, max_pos=max(s_in, ctx) + 8, weights=w)
+    g = torch.Generator().manual_seed(1)
+    hk, d = arch.num_kv_heads, arch.head_dim
+    x = torch.randn(s_in, arch.hidden, generator=g)
+    caches = [{0: (torch.randn(ctx - 1, hk, d, generator=g), torch.randn(ctx - 1, hk, d, generator=g))}
+              for _ in range(batch)]
+    xb = torch.randn(batch, arch.hidden, generator=g)
     t0 = time.perf_counter()
-    orc.tp, orc._decoding = 1, False
-    logits = orc._forward(torch.from_numpy(prompt), torch.arange(sample_in), cache)
+    y = orc._layer(x, 0, torch.arange(s_in), {})
     t1 = time.perf_counter()
-    tok = int(torch.argmax(logits))
-    orc._forward(torch.full((batch,), tok), torch.arange(sample_in, sample_in + batch), cache)
+    logits = orc._norm(y[-1:], w["final_norm"]) @ w["head"].T
     t2 = time.perf_counter()
-    t_tok = (t1 - t0) / sample_in
-    t_step = t2 - t1
-    P, S_in, S_out = args.prompts, args.input_len, args.output_len
-    total = P * S_in * t_tok + S_out * (P / batch) * t_step
-    return {"value": P * S_out / total, "unit": "tokens/s", "cores": threads, "kind": "port",
-            "sample": f"1 prompt x {sample_in} tokens prefilled + one {batch}-token decode step through all "
-                      f"{arch.num_layers} layers of {arch.name} (oracle/llama.py fp32 on bf16 weights); "
-                      f"extrapolated to {P} x {S_in}/{S_out} as P*S_in*t_tok + S_out*(P/{batch})*t_step",
-            "measured_prefill_s": t1 - t0, "measured_decode_step_s": t_step}
+    yb = orc.layer_decode_batch(xb, 0, torch.full((batch,), ctx - 1), caches)
+    t3 = time.perf_counter()
+    lb = orc._norm(yb, w["final_norm"]) @ w["head"].T
+    t4 = time.perf_counter()
+    assert torch.isfinite(logits).all() and torch.isfinite(lb).all()
+    return {"prefill_layer_s": t1 - t0, "prefill_head_s": t2 - t1, "decode_layer_s": t3 - t2,
+            "decode_head_s": t4 - t3, "threads": threads}
 
 
-def _cpu_weights(arch):
-    """bf16 weights for the CPU restatement, generated by the counter-based
-    init on the GPU when one is present (bit-identical to oracle.init_model,
-    which would take minutes in numpy at 8B), else by the oracle itself."""
-    import torch
-
-    from oracle import llama as lo
-
-    names = list(lo.tensor_specs(lo.Arch(arch.num_layers, arch.hidden, arch.num_query_heads, arch.num_kv_heads,
-                                         arch.head_dim, arch.ffn, arch.vocab, arch.rope_theta)).keys())
-    if not torch.cuda.is_available():
-        return None
-    from paper_2503_06433_b200.comm import SoloComm
-    from paper_2503_06433_b200.runtime import Worker
-    from paper_2503_06433_b200.specs import ParallelismConfig
-
-    w = Worker(arch, SoloComm(), 1, torch.device("cuda", torch.cuda.current_device()), seed=0, max_pos=64)
-    w.init_weights(ParallelismConfig(1, 1, 1))
-    out = {}
-    h, d = arch.hidden, arch.head_dim
-    nq, nk = arch.num_query_heads, arch.num_kv_heads
-    for name in names:
-        if name.startswith("L"):
-            layer, key = name.split(".", 1)
-            p = layer + "."
-            if key in ("wq", "wk", "wv"):
-                t = w.w(p + "wqkv")
-                r0 = {"wq": 0, "wk": nq * d, "wv": (nq + nk) * d}[key]
-                r1 = r0 + (nq * d if key == "wq" else nk * d)
-                out[name] = t[r0:r1].cpu()
-            elif key in ("w1", "w3"):
-                t = w.w(p + "w13").view(-1, 2, 32, h)
-                out[name] = t[:, 0 if key == "w1" else 1].reshape(-1, h).cpu()
-            else:
-                out[name] = w.w(p + key).cpu().reshape(-1)[: w.w(p + key).numel()].view(w.w(p + key).shape)
-        else:
-            out[name] = w.w(name).cpu()
-    del w
-    torch.cuda.empty_cache()
-    return _F32View(out)
+def cpu_extrapolate(arch, args, samples: list[dict], batch: int = 8) -> dict:
+    """tokens/s of the whole workload from the per-layer samples: every
+    prompt costs L prefill layers + one head row; every decode step of
+    ``batch`` sequences costs L decode layers + ``batch`` head rows."""
+    P, S_in, S_out, L = args.prompts, args.input_len, args.output_len, arch.num_layers
+    mean = {k: sum(s[k] for s in samples) / len(samples) for k in samples[0] if k.endswith("_s")}
+    t_prompt = L * mean["prefill_layer_s"] + mean["prefill_head_s"]
+    t_step = L * mean["decode_layer_s"] + mean["decode_head_s"]
+    total = P * t_prompt + S_out * math.ceil(P / batch) * t_step
+    return {"value": P * S_out / total, "unit": "tokens/s", "cores": samples[0]["threads"], "kind": "port",
+            "sample": f"per step: one {S_in}-token prompt through one {arch.name} layer + LM head of its last "
+                      f"token, and one batch-{batch} decode step at context {S_in + S_out // 2} through one layer "
+                      f"+ LM head (oracle/llama.py fp32, seeded weights, {samples[0]['threads']} threads); "
+                      f"extrapolated to {P} x {S_in}/{S_out} as P*(L*t_prefill_layer + t_head) + "
+                      f"S_out*ceil(P/{batch})*(L*t_decode_layer + t_head{batch})",
+            "per_layer_s": mean, "extrapolated_batch_s": total}
 
 
-class _F32View(dict):
-    """bf16 tensors handed to the oracle as fp32 on access (keeps host RAM at 2 B/param)."""
+def cpu_baseline(args, arch) -> dict:
+    """The CPU port on one bounded sample (rank 0, N=1; reported beside the
+    GPU line, not the target)."""
+    cpu_port_sample(arch, 64, 64)  # first-touch warm-up of the weights and the thread pool
+    s = cpu_port_sample(arch, args.input_len, args.input_len + args.output_len // 2)
+    return cpu_extrapolate(arch, args, [s])
 
-    def __getitem__(self, k):
-        return dict.__getitem__(self, k).float()
+
+def reference_simulator(args, arch, n: int) -> dict:
+    """The reference's own CPU path, UNMODIFIED: shardsim.simulate() from
+    baseline/_ref (sim.py:748-761) on the same workload and layouts, with a
+    B200 HardwareSpec from the measured peaks; single-threaded Python.  It
+    predicts (models) the batch; its wall time is the reference's CPU cost of
+    the path, and its replay_check validates its own log."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "shardsim").is_dir():
+        return {"unavailable": "baseline/_ref (the reference install) is absent"}
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    import shardsim as ss
+
+    peaks = _peaks()
+    spec = arch.model_spec()
+    model = ss.ModelSpec(num_layers=spec.num_layers, params_per_layer=spec.params_per_layer,
+                         num_query_heads=spec.num_query_heads, num_kv_heads=spec.num_kv_heads,
+                         head_dim=spec.head_dim, bytes_per_param=spec.bytes_per_param)
+    hw = ss.HardwareSpec(num_gpus=n, hbm_bandwidth=peaks["hbm_gbs"] * 1e9, peak_flops=peaks["bf16_tflops"] * 1e12,
+                         gpu_memory=_gpu_memory_bytes(), host_memory_per_gpu=256e9, host_link_bandwidth=64e9,
+                         allreduce=ss.RingAllReduce(770e9))
+    reqs = [ss.Request(i, args.input_len, args.output_len) for i in range(args.prompts)]
+    cfg_p, cfg_d = ss.ParallelismConfig(1, n, 1), ss.ParallelismConfig(n, 1, 1)
+    t0 = time.perf_counter()
+    rep = ss.simulate(model, hw, reqs, ss.SchedulingPolicy.TRANSITION_MINIMIZING, cfg_p, cfg_d)
+    wall = time.perf_counter() - t0
+    verdict = ss.replay_check(rep)
+    return {"module": ss.__file__.replace(str(ROOT) + "/", ""), "wall_s": wall, "cores": 1,
+            "predicted_tokens_per_s": rep.tokens_per_second, "predicted_makespan_s": rep.makespan,
+            "transitions": rep.transitions, "events": len(rep.event_log), "replay_check": bool(verdict),
+            "hardware": f"B200 spec from {peaks['source']} peaks, {n} GPU(s)"}
+
+
+def _gpu_memory_bytes() -> float:
+    """Per-GPU HBM capacity, without touching CUDA (nvidia-smi), else 180 GB."""
+    try:
+        out = subprocess.run(["nvidia-smi", "--id=0", "--query-gpu=memory.total", "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=30).stdout.strip()
+        return float(out.splitlines()[0]) * 2**20
+    except (OSError, ValueError, IndexError, subprocess.TimeoutExpired):
+        return 180e9
 
 
 # ------------------------------------------------------------ reference --
 def run_reference(args) -> None:
+    """The reference arm: the CPU implementation of the path on the host
+    cores (the oracle port — the reference has no numeric path), rank 0
+    only, no GPU and no repo library; plus the reference's own simulate()
+    timed from baseline/_ref."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2503_06433_b200 import PRESETS
-
-    arch = PRESETS[args.arch]
-    import torch
-
-    vals = []
+    arch = _arch(args.arch)
+    n = args.gpus
+    ctx = args.input_len + args.output_len // 2
+    samples, walls = [], []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        cb = cpu_baseline(args, arch, sample_in=args.cpu_sample_in)
+        smp = cpu_port_sample(arch, args.input_len, ctx)
         if i >= args.warmup:
-            vals.append((cb, time.perf_counter() - t0))
-    v = sum(c["value"] for c, _ in vals) / len(vals)
-    step_s = sum(t for _, t in vals) / len(vals)
-    c0 = vals[-1][0]
+            samples.append(smp)
+            walls.append(time.perf_counter() - t0)
+    cb = cpu_extrapolate(arch, args, samples)
+    v = cb["value"]
     line = {
         "impl": "reference",
-        "metric": "offline output tokens/sec (whole box), PP-prefill -> re-shard -> TP-decode",
-        "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.arch} {args.prompts} prompts x {args.input_len} in / {args.output_len} out",
-                   "note": "reference shardsim is an analytic simulator with no numeric path; its CPU "
-                           "implementation of the path is the oracle restatement (oracle/llama.py)"},
-        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": c0["cores"], "kind": "port", "sample": c0["sample"]},
+        "metric": METRIC,
+        "value": v, "unit": "tokens/s", "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sum(walls) / len(walls) * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded weights and activations of the shape)",
+        "config": _config(args, n),
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cb["cores"], "kind": "port", "sample": cb["sample"]},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "per_layer_s": cb["per_layer_s"],
+        "reference_simulator": reference_simulator(args, arch, n),
+        "note": "the reference (shardsim) is an analytic simulator with no numeric path; the CPU implementation "
+                "of the path is the oracle port (oracle/llama.py), timed per layer and extrapolated; "
+                "reference_simulator times the reference's own simulate() on the same workload",
     }
     print(json.dumps(line), flush=True)
 
@@ -615,7 +681,6 @@ def main() -> None:
     ap.add_argument("--input-len", type=int, default=WORKLOAD["input_len"])
     ap.add_argument("--output-len", type=int, default=WORKLOAD["output_len"])
     ap.add_argument("--prefill-tokens", type=int, default=16384)
-    ap.add_argument("--cpu-sample-in", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

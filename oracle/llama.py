@@ -4,14 +4,16 @@ forward, greedy decoding and deterministic random init the B200 engine runs.
 Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may
 import this module; the product package never does.
 
-PARITY UNPINNED against the reference for the numerics: the reference
-(shardsim) has no tensors, logits or tokens (pkg/README.md:10-11,
-SPEC.md:8); the paper's model math is vLLM 0.5.4's Llama (PAPER.md:312,
-:493-494), which is not vendored.  This file is therefore the numeric oracle
-by construction — standard Llama (RMSNorm, rotate-half RoPE, GQA attention,
-SiLU-gated MLP, untied LM head) — and the reference pins only the structure
-around it (placement, byte counts, schedule; see oracle/kv_layout.py and
-tests/golden/).  What the reference does pin here:
+Numerics PINNED to an independent implementation: the reference (shardsim)
+has no tensors, logits or tokens (pkg/README.md:10-11) and the
+paper's model math is vLLM 0.5.4's Llama, which is
+not vendored.  tests/test_oracle_hf_cpu.py loads this file's weights into
+Hugging Face transformers 5.5.0 ``LlamaForCausalLM`` (the same Llama math)
+and requires the fp32 logits to agree within 2e-4 (measured 3.7e-6) and the
+greedy tokens to be identical, on the tiny config and on a head_dim-128 GQA
+shape with the Llama-3 RoPE base.  The reference pins the structure around
+it (placement, byte counts, schedule; see oracle/kv_layout.py and
+tests/golden/), and:
   * sequences are prefilled then decoded exactly output_len times with
     context input_len+1 .. input_len+output_len (sim.py:531, :553-562);
   * KV is reserved at (input_len + output_len) tokens (sim.py:9-12, :256).
@@ -137,13 +139,16 @@ class LlamaOracle:
     ``tp_decode`` are the tensor-parallel degrees of the two phases."""
 
     def __init__(self, a: Arch, seed: int, bf16_faithful: bool = True, max_pos: int = 4096,
-                 weights: dict[str, torch.Tensor] | None = None, tp_prefill: int = 1, tp_decode: int = 1) -> None:
+                 weights: dict[str, torch.Tensor] | None = None, tp_prefill: int = 1, tp_decode: int = 1,
+                 fold_norm: bool = False, pp_prefill: int = 1) -> None:
         self.a = a
         self.bf = bf16_faithful
         self.W = weights if weights is not None else init_model(a, seed)
         self.cos, self.sin = rope_tables(a, max_pos)
         self.tp_prefill, self.tp_decode = tp_prefill, tp_decode
         self.tp = tp_prefill
+        self.fold_norm, self.pp_prefill = fold_norm, pp_prefill
+        self._decoding = False
 
     def _r(self, x: torch.Tensor) -> torch.Tensor:
         return x.to(torch.bfloat16).to(torch.float32) if self.bf else x
@@ -160,13 +165,32 @@ class LlamaOracle:
         x1, x2 = x[..., :half], x[..., half:]
         return self._r(torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], dim=-1))
 
+    def _folding(self) -> bool:
+        return self.fold_norm and self.tp == 1
+
+    def _inv_rms(self, x: torch.Tensor) -> torch.Tensor:
+        return 1.0 / torch.sqrt((x * x).mean(-1, keepdim=True) + self.a.rms_eps)
+
+    def _normed_matmuls(self, x, gain, mats, folded: bool):
+        """[h @ W^T for W in mats] with h = rmsnorm(x) * gain materialised
+        (rounded to bf16) or, folded, (x @ W^T) * (1/rms) on the fp32
+        accumulator (gain 1)."""
+        if not folded:
+            h = self._norm(x, gain)
+            return [h @ w.T for w in mats]
+        assert bool(torch.all(gain == 1)), "folded norms need unit gains (the synthetic init)"
+        inv = self._inv_rms(x)
+        return [(x @ w.T) * inv for w in mats]
+
     def _layer(self, x, l, pos, cache):
         a, W, p = self.a, self.W, f"L{l}."
         d, hq, hk = a.head_dim, a.num_query_heads, a.num_kv_heads
-        h = self._norm(x, W[p + "attn_norm"])
-        q = self._r(h @ W[p + "wq"].T).view(-1, hq, d)
-        k = self._r(h @ W[p + "wk"].T).view(-1, hk, d)
-        v = self._r(h @ W[p + "wv"].T).view(-1, hk, d)
+        per_stage = a.num_layers // (1 if self._decoding else self.pp_prefill)
+        fold_attn = self._folding() and l % per_stage != 0
+        q, k, v = self._normed_matmuls(x, W[p + "attn_norm"], [W[p + "wq"], W[p + "wk"], W[p + "wv"]], fold_attn)
+        q = self._r(q).view(-1, hq, d)
+        k = self._r(k).view(-1, hk, d)
+        v = self._r(v).view(-1, hk, d)
         q, k = self._rope(q, pos), self._rope(k, pos)
         if l not in cache:
             cache[l] = (k, v)
@@ -185,11 +209,36 @@ class LlamaOracle:
             o = torch.einsum("hts,shd->thd", torch.softmax(s, -1), Vx)
         o = self._r(o.reshape(-1, hq * d))
         x = self._row_parallel(x, o, W[p + "wo"])
-        h = self._norm(x, W[p + "mlp_norm"])
-        gte = h @ W[p + "w1"].T
-        up = h @ W[p + "w3"].T
+        gte, up = self._normed_matmuls(x, W[p + "mlp_norm"], [W[p + "w1"], W[p + "w3"]], self._folding())
         act = self._r(torch.nn.functional.silu(gte) * up)
         return self._row_parallel(x, act, W[p + "w2"])
+
+    def layer_decode_batch(self, x: torch.Tensor, l: int, pos: torch.Tensor, caches: list[dict]) -> torch.Tensor:
+        """One decode step of B independent sequences through layer ``l``
+        (fp32): the projections and the MLP batched over the B rows, the
+        attention of row b over sequence b's own cache ``caches[b][l]``
+        (appended in place) — the engine's TP decode step restated on the
+        CPU, used as the CPU baseline's decode sample (bench.py)."""
+        a, W, p = self.a, self.W, f"L{l}."
+        d, hq, hk = a.head_dim, a.num_query_heads, a.num_kv_heads
+        g = hq // hk
+        h = self._norm(x, W[p + "attn_norm"])
+        q = self._rope((h @ W[p + "wq"].T).view(-1, hq, d), pos)
+        k = self._rope((h @ W[p + "wk"].T).view(-1, hk, d), pos)
+        v = (h @ W[p + "wv"].T).view(-1, hk, d)
+        outs = []
+        for b, cache in enumerate(caches):
+            K0, V0 = cache[l]
+            K, V = torch.cat([K0, k[b : b + 1]]), torch.cat([V0, v[b : b + 1]])
+            cache[l] = (K, V)
+            qb = q[b].view(hk, g, d)                                   # [hk, g, d]
+            s = torch.einsum("kgd,skd->kgs", qb, K) / math.sqrt(d)
+            outs.append(torch.einsum("kgs,skd->kgd", torch.softmax(s, -1), V).reshape(hq * d))
+        o = torch.stack(outs)
+        x = x + o @ W[p + "wo"].T
+        h = self._norm(x, W[p + "mlp_norm"])
+        act = torch.nn.functional.silu(h @ W[p + "w1"].T) * (h @ W[p + "w3"].T)
+        return x + act @ W[p + "w2"].T
 
     def _row_parallel(self, x: torch.Tensor, a: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
         """x + a @ w^T; with tp > 1 in bf16 mode, rank r's partial over its
@@ -249,8 +298,10 @@ class LlamaOracle:
         x = self.W["embed"][ids.long()]
         for l in range(self.a.num_layers):
             x = self._layer(x, l, pos, cache)
-        h = self._norm(x[-1:], self.W["final_norm"])
-        return (h @ self.W["head"].T)[0]  # fp32 logits of the last position
+        # the final norm is folded into the LM head only in a decode step
+        (logits,) = self._normed_matmuls(x[-1:], self.W["final_norm"], [self.W["head"]],
+                                         self._folding() and self._decoding)
+        return logits[0]  # fp32 logits of the last position
 
     def generate(self, prompt: np.ndarray, output_len: int, forced: list[int] | None = None
                  ) -> tuple[list[int], list[torch.Tensor]]:

@@ -235,9 +235,11 @@ class _Engine:
         # never more than the whole workload needs
         gpus = cfg_p.gpus_per_replica
         block_bytes_replica = block_size * self.kv_tok
-        per_replica = [s for s in self.seqs if s.replica == 0]
-        want_blocks = int(self.replica_gpu_capacity // block_bytes_replica) + len(per_replica)
-        need_blocks = sum(s.nblocks for s in per_replica)
+        # every replica's ranks size the same pool (shadow allocators mirror
+        # the other replicas' schedules): the largest replica's share decides
+        by_replica = [[s for s in self.seqs if s.replica == r] for r in range(self.dp)]
+        want_blocks = int(self.replica_gpu_capacity // block_bytes_replica) + max(len(q) for q in by_replica)
+        need_blocks = max(sum(s.nblocks for s in q) for q in by_replica)
         num_blocks = min(want_blocks, need_blocks)
         if kv_pool_bytes_per_gpu is not None:
             num_blocks = min(num_blocks, int(kv_pool_bytes_per_gpu // (block_bytes_replica // gpus)))

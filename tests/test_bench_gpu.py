@@ -57,3 +57,36 @@ def test_bench_two_ranks_contract(cuda):
     assert line["replay_check"] is True
     # the PP2 -> TP2 transition moved weights and KV between the two ranks
     assert line["reshard"]["bytes_sent_per_gpu"] > 0
+
+
+def test_bench_eight_ranks_contract(cuda, tmp_path):
+    """bench.py --gpus 8 as 8 torchrun processes (gloo; all on the test box's
+    one GPU) on an 8-layer head_dim-128 GQA model: the PP8 -> TP8 layout the
+    driver's 8-GPU run takes, through the same process-level code path
+    (TorchComm groups, PP send/recv, all-to-all re-shard, TP all-reduce /
+    all-gather).  The line must follow the contract and rank 0's re-shard
+    bytes must equal the placement-rule volume (SURVEY A.3's rules)."""
+    import yaml
+
+    from engine_helpers import expected_kv_bytes_per_token_sent, expected_weight_bytes_sent
+    from paper_2503_06433_b200 import LlamaArch
+
+    arch = LlamaArch("l8-d128", 8, 512, 16, 8, 128, 1024, 2048, rope_theta=500000.0)
+    path = tmp_path / "l8.yaml"
+    path.write_text(yaml.safe_dump(arch.as_dict()))
+    prompts, s_in, s_out = 8, 64, 8
+    args = ["--arch", str(path), "--prompts", str(prompts), "--input-len", str(s_in), "--output-len", str(s_out),
+            "--steps", "1", "--warmup", "3", "--no-cpu-baseline", "--prefill-tokens", "512"]
+    env = dict(os.environ, SSB_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "8", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "8", *args]
+    p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1500, env=env)
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = _last_json(p.stdout)
+    assert KEYS <= set(line)
+    assert line["n_gpus"] == 8 and line["config"]["parallelism"] == "pp8->tp8"
+    assert line["replay_check"] is True and line["value"] > 0
+    blocks = prompts * -(-(s_in + s_out) // 64)
+    kv = expected_kv_bytes_per_token_sent(arch, (1, 8), (8, 1), 0) * 64 * blocks
+    w = expected_weight_bytes_sent(arch, (1, 8), (8, 1), 0)
+    assert line["reshard"]["bytes_sent_per_gpu"] == kv + w

@@ -13,8 +13,6 @@ Checks, against the CPU oracle:
 
 from __future__ import annotations
 
-import threading
-
 import numpy as np
 import pytest
 import torch
@@ -27,41 +25,11 @@ from paper_2503_06433_b200.engine import synthetic_prompts
 from paper_2503_06433_b200.layout import logical_tensors
 from paper_2503_06433_b200.report import SchedulingPolicy
 from paper_2503_06433_b200.runtime import Worker
-from paper_2503_06433_b200.specs import HardwareSpec, ParallelismConfig, Request, RingAllReduce
+from paper_2503_06433_b200.specs import ParallelismConfig, Request
+
+from engine_helpers import check_greedy, oracle_arch, run_threads, tiny_hw  # noqa: F401 (re-exported)
 
 pytestmark = pytest.mark.gpu
-
-
-def tiny_hw(n: int, gpu_memory: float = 2e9, host_memory_per_gpu: float = 2e9) -> HardwareSpec:
-    return HardwareSpec(num_gpus=n, hbm_bandwidth=8e12, peak_flops=2.25e15, gpu_memory=gpu_memory,
-                        host_memory_per_gpu=host_memory_per_gpu, host_link_bandwidth=64e9,
-                        allreduce=RingAllReduce(9e11))
-
-
-def oracle_arch(a) -> lo.Arch:
-    return lo.Arch(a.num_layers, a.hidden, a.num_query_heads, a.num_kv_heads, a.head_dim, a.ffn, a.vocab,
-                   a.rope_theta, a.rms_eps)
-
-
-def run_threads(n, fn):
-    out, errs = [None] * n, []
-
-    def body(r):
-        try:
-            torch.cuda.set_device(0)
-            out[r] = fn(r)
-        except BaseException as e:  # noqa: BLE001
-            errs.append(e)
-            raise
-
-    ts = [threading.Thread(target=body, args=(r,)) for r in range(n)]
-    for t in ts:
-        t.start()
-    for t in ts:
-        t.join(timeout=600)
-    if errs:
-        raise errs[0]
-    return out
 
 
 def _run_tiny(arch_name: str, cfg_p, cfg_d, n_req=8, s_in=64, s_out=32, gpu_seqs=None, p2p=False):
@@ -173,46 +141,33 @@ def test_kv_pool_bit_exact_after_reshard(tiny_run, tiny_run_p2p, which):
         np.testing.assert_array_equal(got[blocks], expect[r][blocks])
 
 
-# Greedy identity criterion.  GPU and oracle both compute in bf16 with fp32
-# accumulation; different (equally valid) fp32 summation orders flip ~0.05% of
-# bf16 roundings, which moves the logits by up to ~0.02 (std ~1).  A step's
-# greedy token is therefore REQUIRED to be identical whenever the oracle's
-# top-1/top-2 margin exceeds that bound; below it both tokens are correct
-# greedy choices at bf16 precision (a "near tie") and either is accepted.
-NEAR_TIE = 0.02
-
-
-def check_greedy(arch, reqs, prompts, outputs, tp_prefill, tp_decode):
-    oracle = lo.LlamaOracle(oracle_arch(arch), seed=0, bf16_faithful=True, max_pos=256,
-                            tp_prefill=tp_prefill, tp_decode=tp_decode)
-    steps = ties = 0
-    for r, p in zip(reqs, prompts):
-        got = outputs[r.id]
-        assert len(got) == r.output_len
-        # teacher forcing: the oracle consumes the GPU's tokens as inputs
-        exp, logs = oracle.generate(p, r.output_len, forced=got)
-        for k, (g, e, lg) in enumerate(zip(got, exp, logs)):
-            steps += 1
-            top2 = torch.topk(lg, 2).values
-            margin = float(top2[0] - top2[1])
-            if g != e:
-                assert margin < NEAR_TIE, f"seq {r.id} step {k}: gpu {g} != oracle {e} with margin {margin:.4f}"
-                assert float(top2[0] - lg[g]) < NEAR_TIE
-                ties += 1
-        # free running: identical until the first near tie on the shared path
-        free, flogs = oracle.generate(p, r.output_len)
-        for k, (g, e, lg) in enumerate(zip(got, free, flogs)):
-            top2 = torch.topk(lg, 2).values
-            if float(top2[0] - top2[1]) < NEAR_TIE:
-                break
-            assert g == e, f"seq {r.id} free-running step {k}: {g} != {e}"
-    assert ties <= 0.03 * steps, f"{ties} near-tie substitutions in {steps} steps"
-    return ties, steps
-
-
 def test_greedy_tokens_match_oracle(tiny_run):
+    """BASELINE configs[0] (8 x 64/32, PP2 -> TP2): greedy tokens against the
+    bf16-faithful oracle, teacher forced.  The GPU's logits of every step are
+    recorded, so each step's actual GPU-vs-oracle deviation is known: a token
+    may differ only at a step whose oracle top-1/top-2 margin is below that
+    step's measured deviation (a tie at the computation's precision), at most
+    1 % of the steps.  The substitutions, the smallest margin and the
+    deviation distribution are printed for the record."""
     arch, reqs, prompts, res, _ = tiny_run
-    check_greedy(arch, reqs, prompts, res[0][0].outputs, 1, 2)
+    rep, wk = res[1]  # rank 1 = last PP stage: prefill and decode logits
+    logs = wk.logit_log
+    n = len(reqs)
+    prefill, decode = torch.cat(logs[:n]), logs[n:]
+    orc = lo.LlamaOracle(oracle_arch(arch), seed=0, bf16_faithful=True, max_pos=256, tp_prefill=1, tp_decode=2,
+                         fold_norm=True, pp_prefill=2)
+    dev = {}
+    for i, (r, p) in enumerate(zip(reqs, prompts)):
+        _, ref = orc.generate(p, r.output_len, forced=rep.outputs[r.id])
+        got = [prefill[i]] + [decode[k][i] for k in range(r.output_len - 1)]
+        for k, (g, e) in enumerate(zip(got, ref)):
+            dev[(r.id, k)] = (g - e).abs().max().item()
+    stats = check_greedy(arch, reqs, prompts, rep.outputs, 1, 2, pp_prefill=2, deviations=dev)
+    assert stats["steps"] == sum(r.output_len for r in reqs) == 256
+    d = np.array(list(dev.values()))
+    print(f"configs[0]: {stats['steps']} greedy steps, {len(stats['substitutions'])} near-tie substitutions "
+          f"{stats['substitutions']}; smallest oracle margin {stats['min_margin']:.5f}; GPU-vs-oracle logit "
+          f"deviation median {np.median(d):.5f} p99 {np.quantile(d, 0.99):.5f} max {d.max():.5f}")
 
 
 def test_p2p_reshard_same_tokens_and_bytes(tiny_run, tiny_run_p2p):
@@ -261,7 +216,7 @@ def test_host_tier_event_log(tiered_run):
 
 def test_host_tier_greedy_tokens(tiered_run):
     arch, reqs, prompts, res, _ = tiered_run
-    check_greedy(arch, reqs, prompts, res[0][0].outputs, 1, 2)
+    check_greedy(arch, reqs, prompts, res[0][0].outputs, 1, 2, pp_prefill=2)
 
 
 def test_host_tier_single_gpu(cuda):
@@ -324,7 +279,7 @@ def test_ragged_lengths_pp2_to_tp2(cuda, gpu_seqs):
     assert rep.outputs == res[1].outputs
     if gpu_seqs is not None:
         assert rep.config["host_tier"]
-    check_greedy(arch, reqs, prompts, rep.outputs, 1, 2)
+    check_greedy(arch, reqs, prompts, rep.outputs, 1, 2, pp_prefill=2)
 
 
 def test_ragged_lengths_llama_shape_single_gpu(cuda):
@@ -439,21 +394,27 @@ def test_folded_norm_matches_rmsnorm_path(cuda, arch_name):
     (rb, lb), (rf, lf) = base[0], fold[0]
     assert replay_check(rf), replay_check(rf).violation
     assert len(lb) == len(lf)
-    # records are in step order; compare them until the first token that
-    # differs (a near tie flips it and the continuations diverge)
-    steps = 0
-    for a, b in zip(lb, lf):
+    # record 0 = the packed prefill of every prompt (rows in request order);
+    # record k >= 1 = decode step k-1, whose rows are the requests with
+    # output_len >= k in request order.  A request whose greedy token flipped
+    # (a near tie) continues from a different token: its later rows are
+    # excluded, every other row is compared in every record.
+    flipped: set[int] = set()
+    rows_compared = 0
+    for k, (a, b) in enumerate(zip(lb, lf)):
+        alive = [r.id for r in reqs if k == 0 or r.output_len >= k]
+        assert a.shape == b.shape and a.shape[0] == len(alive)
         scale = a.abs().max().item()
-        assert a.shape == b.shape
-        assert (a - b).abs().max().item() < 3e-2 * scale + 1e-3
-        flip = (a.argmax(1) != b.argmax(1)).nonzero().flatten()
-        if len(flip):
-            # the first flipped token must be a near tie of the reference
-            top2 = a[flip].topk(2, dim=1).values
-            assert bool(((top2[:, 0] - top2[:, 1]) < 3e-2 * scale).all())
-            break
-        steps += 1
-    # (steps may be 0: a near tie in the very first, prefill, record; its
-    # logits were still checked row by row above)
+        for i, rid in enumerate(alive):
+            if rid in flipped:
+                continue
+            assert (a[i] - b[i]).abs().max().item() < 3e-2 * scale + 1e-3, (k, rid)
+            rows_compared += 1
+            if int(a[i].argmax()) != int(b[i].argmax()):
+                top2 = a[i].topk(2).values
+                assert float(top2[0] - top2[1]) < 3e-2 * scale, (k, rid)
+                flipped.add(rid)
+    # every request's prefill row plus at least half of all decode rows
+    assert rows_compared >= len(reqs) + sum(r.output_len for r in reqs) // 2, (rows_compared, flipped)
     if arch_name == "tiny":
         check_greedy(PRESETS[arch_name], reqs, synthetic_prompts(reqs, PRESETS[arch_name].vocab), rf.outputs, 1, 1)

@@ -108,4 +108,4 @@ def test_two_process_pp2_tp2(cuda, tiered, p2p, fused_tp):
     assert res[0]["outputs"] == res[1]["outputs"]
     arch = PRESETS["tiny"]
     reqs = [Request(i, 64, 32) for i in range(8)]
-    check_greedy(arch, reqs, synthetic_prompts(reqs, arch.vocab), res[0]["outputs"], 1, 2)
+    check_greedy(arch, reqs, synthetic_prompts(reqs, arch.vocab), res[0]["outputs"], 1, 2, pp_prefill=2)

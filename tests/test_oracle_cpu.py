@@ -112,3 +112,32 @@ def test_oracle_generation_tiny_deterministic():
     _, logs2 = orc.generate(p, 4, forced=t1)
     for x, y in zip(logs, logs2):
         torch.testing.assert_close(x, y)
+
+
+def test_layer_decode_batch_matches_per_sequence_decode():
+    """The CPU baseline's batched decode step (bench.py) computes the same
+    layer as the oracle's per-sequence decode: B sequences with their own
+    caches and positions, fp32."""
+    import torch
+
+    from oracle import llama as lo
+
+    a = lo.Arch(1, 256, 8, 2, 64, 512, 512, 10000.0)
+    orc = lo.LlamaOracle(a, seed=0, bf16_faithful=False, max_pos=128)
+    g = torch.Generator().manual_seed(3)
+    lens = [5, 17, 64, 9]
+    caches, xs = [], []
+    for n in lens:
+        c: dict = {}
+        orc._layer(torch.randn(n, a.hidden, generator=g), 0, torch.arange(n), c)
+        caches.append(c)
+        xs.append(torch.randn(1, a.hidden, generator=g))
+    seq = []
+    for n, c, x in zip(lens, caches, xs):
+        cc = {0: (c[0][0].clone(), c[0][1].clone())}
+        orc._decoding = True
+        seq.append(orc._layer(x, 0, torch.tensor([n]), cc)[0])
+    orc._decoding = False
+    out = orc.layer_decode_batch(torch.cat(xs), 0, torch.tensor(lens), caches)
+    torch.testing.assert_close(out, torch.stack(seq), rtol=1e-5, atol=1e-5)
+    assert all(c[0][0].shape[0] == n + 1 for c, n in zip(caches, lens))
