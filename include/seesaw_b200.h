@@ -269,9 +269,13 @@ int ssb_rmsnorm(const void* x, int ldx, const int32_t* row_idx, const void* w, v
  *   sig[r]   ssb_tp_signal_bytes() of zero-initialised device memory per rank
  * Rank r reduces rows [r*rows/n, (r+1)*rows/n) and stores them to every rank.
  * All ranks must make the same calls with the same (rows, hidden, ld,
- * max_blocks) and a per-call epoch that starts at 1 and grows by one; the
- * call synchronises with the peers on the device (no host round trip).  A
- * peer missing for 30 s sets *err = 1 (traps if err is NULL).
+ * max_blocks).  epoch 0 (what the engine passes): the epochs live in the
+ * signal buffer, one counter per CTA index, advanced by the kernel itself —
+ * so a call captured in a CUDA graph stays correct at every replay.  A
+ * non-zero epoch (starting at 1, growing by one per call, never mixed with
+ * epoch-0 calls on the same signal buffer) is taken from the host instead.
+ * The call synchronises with the peers on the device (no host round trip).
+ * A peer missing for 30 s sets *err = 1 (traps if err is NULL).
  * hidden <= 8192, nranks <= 8.
  * ---------------------------------------------------------------------- */
 size_t ssb_tp_signal_bytes(void);
@@ -279,6 +283,16 @@ int ssb_tp_allreduce_rmsnorm(const uint64_t* part_addrs, const uint64_t* x_addrs
                              const uint64_t* sig_addrs, int nranks, int rank, int rows, int hidden, int ld,
                              const void* gamma, float eps, uint32_t epoch, int max_blocks, uint32_t* err,
                              void* stream);
+
+/* Vocab-parallel greedy token of every row across the TP group over peer
+ * memory (replaces the (max, idx) all-gathers + ssb_argmax_combine the
+ * reference's TP decode implies): keys[r] is rank r's uint64 [rows] from
+ * ssb_gemm_lm_head_argmax (orderable logit << 32 | ~global index); out_idx
+ * [rows] receives the index of the largest key over all ranks (the largest
+ * logit, lowest index on ties).  Same signal buffer, epoch and error rules
+ * as ssb_tp_allreduce_rmsnorm (the two share the per-CTA epoch counters). */
+int ssb_tp_argmax_keys(const uint64_t* key_addrs, const uint64_t* sig_addrs, int nranks, int rank, int rows,
+                       int32_t* out_idx, uint32_t epoch, int max_blocks, uint32_t* err, void* stream);
 
 /* Decode-step bookkeeping on device: ctx_lens[b] += 1; positions[b] =
  * ctx_lens[b]-1; slots[b] = block_tables[b][pos/bs]*bs + pos%bs. */

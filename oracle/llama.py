@@ -136,18 +136,29 @@ class LlamaOracle:
     epilogue), and attention runs the kernels' online softmax — 64-key tiles
     in prefill, per-warp 16-key slices of 64-token pool blocks in decode —
     with bf16 probabilities entering the PV product.  ``tp_prefill`` /
-    ``tp_decode`` are the tensor-parallel degrees of the two phases."""
+    ``tp_decode`` are the tensor-parallel degrees of the two phases.
+
+    ``fold_norm`` mirrors the engine's default path (runtime.Worker.
+    _block_folded, SSB_FOLD_NORM=1): in a phase whose tensor parallelism is
+    1, the norm in front of a projection is not materialised — the projection
+    consumes x and its fp32 accumulator rows are scaled by 1/rms before the
+    bf16 rounding (gains are 1 in the synthetic init, so folding them into
+    the weights is the identity).  The exceptions are the engine's: the
+    attention norm of a stage's first layer (the stage's input arrives
+    without row sums) and the final norm of a prefill (last-token rows) run
+    as rmsnorm kernels.  ``pp_prefill`` / ``pp_decode`` give the stage
+    boundaries of the two phases."""
 
     def __init__(self, a: Arch, seed: int, bf16_faithful: bool = True, max_pos: int = 4096,
                  weights: dict[str, torch.Tensor] | None = None, tp_prefill: int = 1, tp_decode: int = 1,
-                 fold_norm: bool = False, pp_prefill: int = 1) -> None:
+                 fold_norm: bool = False, pp_prefill: int = 1, pp_decode: int = 1) -> None:
         self.a = a
         self.bf = bf16_faithful
         self.W = weights if weights is not None else init_model(a, seed)
         self.cos, self.sin = rope_tables(a, max_pos)
         self.tp_prefill, self.tp_decode = tp_prefill, tp_decode
         self.tp = tp_prefill
-        self.fold_norm, self.pp_prefill = fold_norm, pp_prefill
+        self.fold_norm, self.pp_prefill, self.pp_decode = fold_norm, pp_prefill, pp_decode
         self._decoding = False
 
     def _r(self, x: torch.Tensor) -> torch.Tensor:
@@ -185,7 +196,7 @@ class LlamaOracle:
     def _layer(self, x, l, pos, cache):
         a, W, p = self.a, self.W, f"L{l}."
         d, hq, hk = a.head_dim, a.num_query_heads, a.num_kv_heads
-        per_stage = a.num_layers // (1 if self._decoding else self.pp_prefill)
+        per_stage = a.num_layers // (self.pp_decode if self._decoding else self.pp_prefill)
         fold_attn = self._folding() and l % per_stage != 0
         q, k, v = self._normed_matmuls(x, W[p + "attn_norm"], [W[p + "wq"], W[p + "wk"], W[p + "wv"]], fold_attn)
         q = self._r(q).view(-1, hq, d)

@@ -98,6 +98,7 @@ SIGNATURES: dict[str, list] = {
     "ssb_decode_attention": [_P, _I, _I, _I, _P, KVGeometry, _I, _I, _P, _I, _P, _I, _P, _I, _F, _P],
     "ssb_tp_allreduce_rmsnorm": [_PU64, _PU64, _PU64, _PU64, _I, _I, _I, _I, _I, _P, _F, ctypes.c_uint32, _I, _P,
                                  _P],
+    "ssb_tp_argmax_keys": [_PU64, _PU64, _I, _I, _I, _P, ctypes.c_uint32, _I, _P, _P],
 }
 
 _lock = threading.Lock()

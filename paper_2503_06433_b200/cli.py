@@ -86,6 +86,9 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--events-csv", help="write the event log to this CSV file")
     p.add_argument("--outputs", help="write generated token ids (JSON) to this file")
+    p.add_argument("--tm-mode", choices=["native", "reference"], default="native",
+                   help="transition-minimizing: keep fitting KV in HBM (native) or route every wave "
+                        "through the host tier (the reference's schedule)")
 
     p = sub.add_parser("plan", help="shard maps, reload plan and NVLink exchange of a layout switch")
     p.add_argument("--model", required=True)
@@ -126,17 +129,21 @@ def _cmd_execute(args) -> int:
                          seed=args.seed)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % max(torch.cuda.device_count(), 1))
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # SSB_DIST_BACKEND=gloo: ranks sharing one GPU (multi-rank test runs)
+        if os.environ.get("SSB_DIST_BACKEND", "nccl") == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
         comm = TorchComm()
     else:
         comm = SoloComm()
     rep = execute(model, hw, reqs, _POLICIES[args.policy], ParallelismConfig.parse(args.prefill_cfg),
                   ParallelismConfig.parse(args.decode_cfg), options, arch=arch, seed=args.seed, prompts=prompts,
-                  comm=comm)
+                  comm=comm, tm_mode=args.tm_mode)
     verdict = replay_check(rep)
     if not verdict:
         raise RuntimeError(f"replay check failed: {verdict.violation}")

@@ -59,10 +59,13 @@ class Comm:
         shared host KV tier).  Collective."""
         raise NotImplementedError
 
-    def peer_addresses(self, t: torch.Tensor) -> list[int]:
+    def peer_addresses(self, t: torch.Tensor, keep: list) -> list[int]:
         """Device addresses, valid in THIS process, of every member's ``t``
         (the tensor each member passes): the local pointer for self, CUDA IPC
-        mappings (NVLink peer memory) for the others.  Collective."""
+        mappings (NVLink peer memory) for the others.  The objects that keep
+        the mappings open are appended to ``keep``: the caller owns them (the
+        buffer's owner), so a mapping closes when its owner is released.
+        Collective."""
         raise NotImplementedError
 
 
@@ -101,7 +104,7 @@ class SoloComm(Comm):
     def share_host_buffer(self, nbytes: int) -> torch.Tensor:
         return _pinned(nbytes)
 
-    def peer_addresses(self, t: torch.Tensor) -> list[int]:
+    def peer_addresses(self, t: torch.Tensor, keep: list) -> list[int]:
         return [t.data_ptr()]
 
 
@@ -195,9 +198,10 @@ class TorchComm(Comm):
         return buf
 
 
-    def peer_addresses(self, t: torch.Tensor) -> list[int]:
+    def peer_addresses(self, t: torch.Tensor, keep: list) -> list[int]:
         """CUDA IPC: every member exports its allocation, the others map it
-        (cudaIpcOpenMemHandle through torch's shared-storage path)."""
+        (cudaIpcOpenMemHandle through torch's shared-storage path); the
+        mapped peer storages go to ``keep``."""
         storage = t.untyped_storage()
         handle = storage._share_cuda_()
         mine = (handle, t.storage_offset() * t.element_size())
@@ -209,13 +213,12 @@ class TorchComm(Comm):
                 addrs.append(t.data_ptr())
                 continue
             peer = torch.UntypedStorage._new_shared_cuda(*h)
-            _IPC_KEEPALIVE.append(peer)
+            keep.append(peer)
             addrs.append(peer.data_ptr() + off)
         return addrs
 
 
 _GROUPS: dict[tuple[int, ...], object] = {}
-_IPC_KEEPALIVE: list = []
 _SHM_KEEPALIVE: list = []
 
 
@@ -226,11 +229,15 @@ def _new_group_cached(dist, ranks: tuple[int, ...]):
 
 
 class _ThreadWorld:
-    """Shared state of W thread-ranks."""
+    """Shared state of W thread-ranks.  Every wait is bounded (TIMEOUT_S):
+    a rank that died leaves the others with BrokenBarrierError / TimeoutError
+    instead of a hang."""
+
+    TIMEOUT_S = 300.0
 
     def __init__(self, size: int) -> None:
         self.size = size
-        self.barrier = threading.Barrier(size)
+        self.barrier = threading.Barrier(size, timeout=self.TIMEOUT_S)
         self.slots: dict = {}
         self.lock = threading.Lock()
         self.mail: dict[tuple[int, int, int], torch.Tensor] = {}
@@ -324,13 +331,15 @@ class ThreadComm(Comm):
             w.mail[key] = t
             w.mail_cv.notify_all()
             # rendezvous: wait until the receiver consumed it (buffer reuse safety)
-            w.mail_cv.wait_for(lambda: key not in w.mail)
+            if not w.mail_cv.wait_for(lambda: key not in w.mail, timeout=w.TIMEOUT_S):
+                raise TimeoutError(f"ThreadComm send {key}: receiver never took it")
 
     def recv(self, t, src) -> None:
         key = self._key(src, self.rank)
         w = self.world
         with w.mail_cv:
-            w.mail_cv.wait_for(lambda: key in w.mail)
+            if not w.mail_cv.wait_for(lambda: key in w.mail, timeout=w.TIMEOUT_S):
+                raise TimeoutError(f"ThreadComm recv {key}: sender never posted it")
             t.copy_(w.mail[key])
             self._sync()
             del w.mail[key]
@@ -345,7 +354,7 @@ class ThreadComm(Comm):
         self._done()
         return buf
 
-    def peer_addresses(self, t: torch.Tensor) -> list[int]:
+    def peer_addresses(self, t: torch.Tensor, keep: list) -> list[int]:
         objs = self._exchange(t.data_ptr())
         self._done()
         return list(objs)

@@ -69,6 +69,20 @@ __device__ __forceinline__ uint64_t global_ns() {
 // Slot layout of a rank's signal buffer: [phase 2][kARMaxBlocks][kARMaxRanks]
 // u32; peer p announces epoch e for (phase, b) by writing slot [phase][b][p]
 // of every rank.  Epochs only grow, so no reset is needed between calls.
+// After the barrier slots: [kARMaxBlocks] u32 of this rank's per-CTA epoch
+// counters, used when the host passes epoch 0 — CTA b of a call takes
+// counter[b] + 1 and stores it back at its end, so the epochs live on the
+// device and a call captured in a CUDA graph advances them at every replay
+// (all ranks launch the same grids in the same order, so CTA b's counter
+// moves in lockstep on every rank).
+constexpr size_t kARSlots = static_cast<size_t>(2) * kARMaxBlocks * kARMaxRanks;
+
+__device__ __forceinline__ uint32_t cta_epoch(const ARPeers& P, int rank, uint32_t host_epoch) {
+  return host_epoch ? host_epoch : *(const volatile uint32_t*)(P.sig[rank] + kARSlots + blockIdx.x) + 1u;
+}
+__device__ __forceinline__ void cta_epoch_done(const ARPeers& P, int rank, uint32_t host_epoch, uint32_t epoch) {
+  if (!host_epoch && threadIdx.x == 0) P.sig[rank][kARSlots + blockIdx.x] = epoch;
+}
 __device__ __forceinline__ bool peer_barrier(const ARPeers& P, int n, int rank, int phase, uint32_t epoch,
                                              uint32_t* err) {
   __threadfence_system();  // this CTA's P2P stores before the announcement
@@ -105,9 +119,13 @@ __device__ __forceinline__ void unpack8(const uint4 v, float* f) {
 template <int N>
 __global__ void __launch_bounds__(kARThreads)
     tp_allreduce_rmsnorm_kernel(ARPeers P, int rank, int rows, int hidden, int ld,
-                                const __nv_bfloat16* __restrict__ gamma, float eps, uint32_t epoch,
+                                const __nv_bfloat16* __restrict__ gamma, float eps, uint32_t host_epoch,
                                 uint32_t* err) {
-  if (!peer_barrier(P, N, rank, 0, epoch, err)) return;
+  const uint32_t epoch = cta_epoch(P, rank, host_epoch);
+  if (!peer_barrier(P, N, rank, 0, epoch, err)) {
+    cta_epoch_done(P, rank, host_epoch, epoch);
+    return;
+  }
   const int r0 = static_cast<int>(static_cast<int64_t>(rows) * rank / N);
   const int r1 = static_cast<int>(static_cast<int64_t>(rows) * (rank + 1) / N);
   const int nvec = hidden / 8;
@@ -182,6 +200,38 @@ __global__ void __launch_bounds__(kARThreads)
     }
   }
   peer_barrier(P, N, rank, 1, epoch, err);
+  cta_epoch_done(P, rank, host_epoch, epoch);
+}
+
+// Vocab-parallel greedy argmax across the TP group: every rank's LM-head
+// epilogue left one packed 64-bit key per row (orderable fp32 logit << 32 |
+// ~global index: the max key is the max logit, lowest index on ties —
+// argmax_combine's rule) in its `keys` buffer.  After barrier A each CTA
+// loads its rows' keys from every rank over NVLink, keeps the max and writes
+// the token id locally; barrier B releases the peers' key buffers.  Replaces
+// the two NCCL all-gathers + combine of the vocab-parallel head.
+struct ARKeys {
+  const unsigned long long* k[kARMaxRanks];
+};
+
+template <int N>
+__global__ void __launch_bounds__(kARThreads)
+    tp_argmax_kernel(ARPeers P, ARKeys keys, int rank, int rows, int32_t* __restrict__ out, uint32_t host_epoch,
+                     uint32_t* err) {
+  const uint32_t epoch = cta_epoch(P, rank, host_epoch);
+  if (peer_barrier(P, N, rank, 0, epoch, err)) {
+    for (int row = blockIdx.x * kARThreads + threadIdx.x; row < rows; row += gridDim.x * kARThreads) {
+      unsigned long long best = 0;
+#pragma unroll
+      for (int p = 0; p < N; ++p) {
+        const unsigned long long k = __ldcg(keys.k[p] + row);
+        best = k > best ? k : best;
+      }
+      out[row] = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(best & 0xFFFFFFFFu));
+    }
+    peer_barrier(P, N, rank, 1, epoch, err);
+  }
+  cta_epoch_done(P, rank, host_epoch, epoch);
 }
 
 }  // namespace
@@ -190,7 +240,7 @@ __global__ void __launch_bounds__(kARThreads)
 extern "C" {
 
 size_t ssb_tp_signal_bytes(void) {
-  return static_cast<size_t>(2) * ssb::kARMaxBlocks * ssb::kARMaxRanks * sizeof(uint32_t);
+  return (ssb::kARSlots + ssb::kARMaxBlocks) * sizeof(uint32_t);
 }
 
 int ssb_tp_allreduce_rmsnorm(const uint64_t* part_addrs, const uint64_t* x_addrs, const uint64_t* h_addrs,
@@ -207,7 +257,6 @@ int ssb_tp_allreduce_rmsnorm(const uint64_t* part_addrs, const uint64_t* x_addrs
   SSB_REQUIRE(ld >= hidden && ld % 8 == 0, "ssb_tp_allreduce_rmsnorm: bad ld %d", ld);
   SSB_REQUIRE(part_addrs && x_addrs && sig_addrs, "ssb_tp_allreduce_rmsnorm: null address table");
   SSB_REQUIRE(!gamma || h_addrs, "ssb_tp_allreduce_rmsnorm: gamma without h buffers");
-  SSB_REQUIRE(epoch != 0, "ssb_tp_allreduce_rmsnorm: epoch 0 is the signal buffers' initial value");
   SSB_REQUIRE(max_blocks >= 1, "ssb_tp_allreduce_rmsnorm: max_blocks %d", max_blocks);
   if (rows == 0) return 0;
   ARPeers P{};
@@ -241,6 +290,43 @@ int ssb_tp_allreduce_rmsnorm(const uint64_t* part_addrs, const uint64_t* x_addrs
 #undef SSB_AR_CASE
   }
   return check_launch("ssb_tp_allreduce_rmsnorm");
+}
+
+int ssb_tp_argmax_keys(const uint64_t* key_addrs, const uint64_t* sig_addrs, int nranks, int rank, int rows,
+                       int32_t* out_idx, uint32_t epoch, int max_blocks, uint32_t* err, void* stream) {
+  using namespace ssb;
+  SSB_REQUIRE(nranks >= 1 && nranks <= kARMaxRanks, "ssb_tp_argmax_keys: nranks %d not in [1, %d]", nranks,
+              kARMaxRanks);
+  SSB_REQUIRE(rank >= 0 && rank < nranks, "ssb_tp_argmax_keys: rank %d of %d", rank, nranks);
+  SSB_REQUIRE(key_addrs && sig_addrs && out_idx && rows >= 0, "ssb_tp_argmax_keys: null argument");
+  SSB_REQUIRE(max_blocks >= 1, "ssb_tp_argmax_keys: max_blocks %d", max_blocks);
+  if (rows == 0) return 0;
+  ARPeers P{};
+  ARKeys K{};
+  for (int p = 0; p < nranks; ++p) {
+    P.sig[p] = reinterpret_cast<uint32_t*>(sig_addrs[p]);
+    K.k[p] = reinterpret_cast<const unsigned long long*>(key_addrs[p]);
+    SSB_REQUIRE(P.sig[p] && K.k[p], "ssb_tp_argmax_keys: rank %d null buffer", p);
+  }
+  // the peers' key pointers travel by value in the kernel's parameter space
+  const int grid = std::min(std::min((rows + kARThreads - 1) / kARThreads, max_blocks), kARMaxBlocks);
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  switch (nranks) {
+#define SSB_AM_CASE(N)                                                                                   \
+  case N:                                                                                                \
+    tp_argmax_kernel<N><<<grid, kARThreads, 0, s>>>(P, K, rank, rows, out_idx, epoch, err);              \
+    break;
+    SSB_AM_CASE(1)
+    SSB_AM_CASE(2)
+    SSB_AM_CASE(3)
+    SSB_AM_CASE(4)
+    SSB_AM_CASE(5)
+    SSB_AM_CASE(6)
+    SSB_AM_CASE(7)
+    SSB_AM_CASE(8)
+#undef SSB_AM_CASE
+  }
+  return check_launch("ssb_tp_argmax_keys");
 }
 
 }  // extern "C"

@@ -199,13 +199,28 @@ class Piece:
     def numel(self) -> int:
         return self.rows * self.cols
 
+    def row_slice(self, k: int, parts: int) -> "Piece | None":
+        """The k-th of ``parts`` row ranges of this piece (None if empty):
+        how a re-partition is streamed in chunks every rank agrees on."""
+        a, b = k * self.rows // parts, (k + 1) * self.rows // parts
+        if b <= a:
+            return None
+        return Piece(self.src_off + a * self.src_ld, self.dst_off + a * self.dst_ld, self.src_ld, self.dst_ld,
+                     b - a, self.cols)
+
 
 def repartition_pieces(src: WeightLayout, dst: WeightLayout) -> list[Piece]:
     """Everything GPU ``src`` holds that GPU ``dst`` needs, in a deterministic
-    order (dst tensor order, then segment order, then src segment order)."""
+    order (dst tensor order, then segment order, then src segment order).
+
+    The norm gains are the only tensors a layout replicates (every tensor
+    rank of a stage holds them whole); they are sent by the stage's rank 0
+    only, so each element of the new layout has exactly one source."""
     by_logical: dict[str, list[tuple[LocalTensor, Segment]]] = {}
     for t in src.tensors.values():
         for s in t.segments:
+            if src.rank != 0 and s.logical.endswith("norm"):
+                continue
             by_logical.setdefault(s.logical, []).append((t, s))
     pieces: list[Piece] = []
     for dt in dst.tensors.values():

@@ -357,6 +357,29 @@ def tp_signal_bytes() -> int:
     return int(load().ssb_tp_signal_bytes())
 
 
+def tp_argmax_keys(key_addrs, sig_addrs, rank: int, rows: int, out_idx: torch.Tensor, epoch: int,
+                   max_blocks: int, err: torch.Tensor | None = None) -> None:
+    """out_idx[r] = token of the largest LM-head key of row r over every
+    rank's keys buffer (peer memory; C-ABI ssb_tp_argmax_keys)."""
+    if out_idx.dtype != torch.int32:
+        raise ValueError("tp_argmax_keys: out_idx must be int32")
+    call("ssb_tp_argmax_keys", _lib.uint64_array(key_addrs), _lib.uint64_array(sig_addrs), len(key_addrs), rank,
+         rows, out_idx.data_ptr(), epoch, max_blocks, err.data_ptr() if err is not None else None, _stream())
+
+
+def lm_head_keys(h: torch.Tensor, w: torch.Tensor, index_base: int, keys: torch.Tensor,
+                 workspace: torch.Tensor | None = None, rownorm: "_lib.RowNorm | None" = None) -> None:
+    """The LM-head GEMM with its argmax epilogue only: keys[r] = packed
+    (logit, index + index_base) maximum of row r (no decode to value/index)."""
+    _check(h, "h")
+    _check(w, "w")
+    M, K = h.shape
+    call("ssb_gemm_lm_head_argmax", h.data_ptr(), w.data_ptr(), M, w.shape[0], K, h.stride(0), w.stride(0),
+         index_base, keys.data_ptr(), 0, 0, workspace.data_ptr() if workspace is not None else None,
+         workspace.numel() * workspace.element_size() if workspace is not None else 0,
+         ctypes.byref(rownorm) if rownorm is not None else None, _stream())
+
+
 def tp_allreduce_rmsnorm(part_addrs, x_addrs, h_addrs, sig_addrs, rank: int, rows: int, hidden: int,
                          gamma: torch.Tensor | None, eps: float, epoch: int, max_blocks: int,
                          err: torch.Tensor | None = None) -> None:

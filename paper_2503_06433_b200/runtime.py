@@ -86,6 +86,7 @@ class Worker:
     """One GPU of the fleet (SPMD)."""
 
     GEMM_WS_BYTES = 64 << 20
+    RESHARD_CHUNK_BYTES = int(__import__("os").environ.get("SSB_RESHARD_CHUNK_MB", "256")) << 20
 
     def __init__(self, arch: LlamaArch, world: Comm, dp: int, device: torch.device, seed: int = 0,
                  block_size: int = 64, max_pos: int = 4096) -> None:
@@ -106,9 +107,11 @@ class Worker:
         self.num_blocks = 0
         self.scale = 1.0 / math.sqrt(arch.head_dim)
         self._comm_cache: dict = {}
+        self._wplans: dict = {}
         self.stream = torch.cuda.current_stream(device) if device.type == "cuda" else None
         self.record_logits = False
         self.logit_log: list[torch.Tensor] = []
+        self.logit_rows: list[list] = []  # request ids of each recorded forward's rows (set by the engine)
         self.stats: dict[str, float] = {}
         # test/inspection callbacks invoked by the engine: name -> fn(worker, **kw)
         self.hooks: dict = {}
@@ -144,6 +147,10 @@ class Worker:
         # GEMMs emit row sums of squares, the consumers scale rows by 1/rms,
         # the gains live in the consumer weights (fold_gains)
         self.fold_norm = os.environ.get("SSB_FOLD_NORM", "1") != "0"
+        # decode steps replayed from CUDA graphs (per batch size)
+        self.cuda_graphs = os.environ.get("SSB_CUDA_GRAPH", "1") != "0"
+        self._graphs: dict = {}
+        self._graph_pool = None
 
     # ------------------------------------------------------------ layouts --
     def _tp_comm(self, cfg: ParallelismConfig, stage: int) -> Comm:
@@ -207,6 +214,7 @@ class Worker:
         """One allocation serves every layout: a block has the same byte size
         under any (tp, pp) with the same tp*pp."""
         self.num_blocks = num_blocks
+        self._drop_graphs()
         geo = self.geometry()
         # zero-filled once: decode attention multiplies the (masked, p = 0)
         # tail of a sequence's last block by its V rows, and never-written
@@ -215,63 +223,194 @@ class Worker:
         self.pool = torch.zeros(num_blocks * geo.block_elems, dtype=torch.bfloat16, device=self.device)
 
     # ------------------------------------------------------- re-partition --
+    def _weight_plan(self, cfg_old: ParallelismConfig, cfg_new: ParallelismConfig):
+        """(pieces[p][q], chunks): what replica GPU p sends to GPU q, and the
+        number of chunks the re-partition streams in — identical on every
+        rank (computed from all layouts), cached per transition."""
+        key = (cfg_old, cfg_new)
+        plan = self._wplans.get(key)
+        if plan is None:
+            n = self.per_replica
+            old = [weight_layout(self.arch, cfg_old.tp, cfg_old.pp, g) for g in range(n)]
+            new = [weight_layout(self.arch, cfg_new.tp, cfg_new.pp, g) for g in range(n)]
+            pieces = [[repartition_pieces(old[p], new[q]) for q in range(n)] for p in range(n)]
+            moved = [sum(pc.numel for q in range(n) if q != p for pc in pieces[p][q]) for p in range(n)]
+            moved += [sum(pc.numel for p in range(n) if p != q for pc in pieces[p][q]) for q in range(n)]
+            chunks = max(1, math.ceil(2 * max(moved) / self.RESHARD_CHUNK_BYTES))
+            plan = self._wplans[key] = (pieces, chunks)
+        return plan
+
     def repartition_weights(self, cfg_new: ParallelismConfig) -> int:
-        """Weight column/row re-partition over the replica group; returns bytes
-        this GPU sent to other GPUs."""
+        """Weight column/row re-partition over the replica group; returns the
+        bytes this GPU sent to other GPUs.
+
+        Streamed in chunks every rank agrees on (the k-th row range of every
+        piece): per chunk, copy2d packs the pieces for every peer into a send
+        buffer, an all-to-all moves them, copy2d unpacks into the new arena;
+        the pack of chunk k+1 overlaps the all-to-all of chunk k.  Pieces this
+        GPU keeps are one direct copy.  Peak HBM: old arena + new arena + two
+        chunk buffers each way (SSB_RESHARD_CHUNK_MB, 256 MiB) — never a full
+        send or receive copy of the shard."""
         old = self.state
+        self._drop_graphs()
+        pieces, K = self._weight_plan(old.cfg, cfg_new)
         new = self.make_layout(cfg_new)
-        n = self.per_replica
-        old_layouts = [weight_layout(self.arch, old.cfg.tp, old.cfg.pp, g) for g in range(n)]
-        new_layouts = [weight_layout(self.arch, cfg_new.tp, cfg_new.pp, g) for g in range(n)]
-        send_entries, recv_entries = [], []
-        send_splits, recv_splits = [], []
+        me, n = self.gpu, self.per_replica
+        keep = pieces[me][me]
+        if keep:
+            d, tot = _copy_desc_rows([(pc.src_off * 2, pc.dst_off * 2, pc.src_ld * 2, pc.dst_ld * 2, pc.rows,
+                                       pc.cols * 2) for pc in keep])
+            ops.copy2d_batched(old.arena, new.arena, torch.from_numpy(d).to(self.device), tot)
+        sent = 2 * sum(pc.numel for q in range(n) if q != me for pc in pieces[me][q])
+        if n > 1 and sent + sum(pc.numel for p in range(n) if p != me for pc in pieces[p][me]):
+            if self.p2p_reshard and self.device.type == "cuda":
+                self._repartition_p2p(old, new, pieces, K)
+            else:
+                self._repartition_a2a(old, new, pieces, K)
+        self.state = new
+        return sent
+
+    def _weight_chunk(self, pieces, k: int, K: int):
+        """Send / receive copy descriptors and splits of chunk k (elements)."""
+        me, n = self.gpu, self.per_replica
+        send, recv, s_splits, r_splits = [], [], [], []
         s_pos = r_pos = 0
         for q in range(n):
-            pieces = repartition_pieces(old_layouts[self.gpu], new_layouts[q])
             start = s_pos
-            for p in pieces:
-                send_entries.append((p.src_off * 2, s_pos * 2, p.src_ld * 2, p.cols * 2, p.rows, p.cols * 2))
-                s_pos += p.numel
-            send_splits.append(s_pos - start)
-            pieces = repartition_pieces(old_layouts[q], new_layouts[self.gpu])
+            for pc in (pieces[me][q] if q != me else ()):
+                sl = pc.row_slice(k, K)
+                if sl is not None:
+                    send.append((sl.src_off * 2, s_pos * 2, sl.src_ld * 2, sl.cols * 2, sl.rows, sl.cols * 2))
+                    s_pos += sl.numel
+            s_splits.append(s_pos - start)
             start = r_pos
-            for p in pieces:
-                recv_entries.append((r_pos * 2, p.dst_off * 2, p.cols * 2, p.dst_ld * 2, p.rows, p.cols * 2))
-                r_pos += p.numel
-            recv_splits.append(r_pos - start)
-        recv = torch.empty(max(r_pos, 8), dtype=torch.bfloat16, device=self.device)
-        rd, rtot = _copy_desc_rows(recv_entries)
-        if self.p2p_reshard and self.device.type == "cuda" and n > 1:
-            # pack + transfer in one kernel: every piece is stored straight into
-            # its owner's receive buffer (IPC peer memory), at the section that
-            # follows the sections of the ranks before this one
-            addrs = self.replica_comm.peer_addresses(recv)
-            p2p_entries = []
+            for pc in (pieces[q][me] if q != me else ()):
+                sl = pc.row_slice(k, K)
+                if sl is not None:
+                    recv.append((r_pos * 2, sl.dst_off * 2, sl.cols * 2, sl.dst_ld * 2, sl.rows, sl.cols * 2))
+                    r_pos += sl.numel
+            r_splits.append(r_pos - start)
+        return send, recv, s_splits, r_splits
+
+    def _repartition_a2a(self, old: LayoutState, new: LayoutState, pieces, K: int) -> None:
+        chunks = []
+        for k in range(K):
+            send, recv, s_splits, r_splits = self._weight_chunk(pieces, k, K)
+            sd, stot = _copy_desc_rows(send)
+            rd, rtot = _copy_desc_rows(recv)
+            chunks.append((torch.from_numpy(sd).to(self.device), stot, s_splits,
+                           torch.from_numpy(rd).to(self.device), rtot, r_splits))
+        cap_s = max(max(sum(c[2]) for c in chunks), 8)
+        cap_r = max(max(sum(c[5]) for c in chunks), 8)
+        cuda = self.device.type == "cuda"
+        nbuf = 2 if cuda and K > 1 else 1
+        sends = [torch.empty(cap_s, dtype=torch.bfloat16, device=self.device) for _ in range(nbuf)]
+        recvs = [torch.empty(cap_r, dtype=torch.bfloat16, device=self.device) for _ in range(nbuf)]
+
+        def pack(k):
+            sd, stot, _, _, _, _ = chunks[k]
+            if stot:
+                ops.copy2d_batched(old.arena, sends[k % nbuf], sd, stot)
+
+        def unpack(k):
+            _, _, _, rd, rtot, _ = chunks[k]
+            if rtot:
+                ops.copy2d_batched(recvs[k % nbuf], new.arena, rd, rtot)
+
+        if not cuda or nbuf == 1:
+            for k in range(K):
+                pack(k)
+                _, _, s_splits, _, _, r_splits = chunks[k]
+                self.replica_comm.all_to_all(recvs[0], sends[0], r_splits, s_splits)
+                unpack(k)
+            return
+        main = torch.cuda.current_stream(self.device)
+        cs = self._comm_stream_()
+        arrived: list = [None] * K
+        free = [None] * nbuf  # event: the chunk that last used buffer b was unpacked
+
+        def launch(k):
+            b = k % nbuf
+            if free[b] is not None:
+                main.wait_event(free[b])
+            pack(k)
+            packed = torch.cuda.Event()
+            packed.record(main)
+            with torch.cuda.stream(cs):
+                cs.wait_event(packed)
+                _, _, s_splits, _, _, r_splits = chunks[k]
+                self.replica_comm.all_to_all(recvs[b], sends[b], r_splits, s_splits)
+                arrived[k] = torch.cuda.Event()
+                arrived[k].record(cs)
+
+        launch(0)
+        for k in range(K):
+            if k + 1 < K:
+                launch(k + 1)
+            main.wait_event(arrived[k])
+            unpack(k)
+            free[k % nbuf] = torch.cuda.Event()
+            free[k % nbuf].record(main)
+        for b in range(nbuf):
+            sends[b].record_stream(cs)
+            recvs[b].record_stream(cs)
+
+    def _comm_stream_(self) -> torch.cuda.Stream:
+        if getattr(self, "_comm_stream", None) is None:
+            self._comm_stream = torch.cuda.Stream(self.device)
+        return self._comm_stream
+
+    def _p2p_buffer(self, elems: int):
+        """This rank's peer-mapped receive buffer (>= elems bf16) and every
+        peer's address of it; one allocation reused by every P2P re-shard and
+        grown collectively (the size is identical on all ranks)."""
+        buf = getattr(self, "_p2p", None)
+        if buf is None or buf[0].numel() < elems:
+            self._p2p = None  # release the old buffer and its peer mappings first
+            t = torch.empty(elems, dtype=torch.bfloat16, device=self.device)
+            maps: list = []
+            self._p2p = (t, self.replica_comm.peer_addresses(t, maps), maps)
+        return self._p2p[0], self._p2p[1]
+
+    def _repartition_p2p(self, old: LayoutState, new: LayoutState, pieces, K: int) -> None:
+        """Pack + transfer in one kernel per chunk: every piece is stored
+        straight into its owner's receive buffer (IPC peer memory), at the
+        section that follows the sections of the ranks before this one."""
+        me, n = self.gpu, self.per_replica
+        per_chunk = []
+        cap = 8
+        for k in range(K):
+            # elements p sends q in chunk k, for every pair (the receivers' layout)
+            sizes = [[sum(sl.numel for pc in pieces[p][q] if p != q for sl in [pc.row_slice(k, K)] if sl)
+                      for q in range(n)] for p in range(n)]
+            cap = max(cap, max(sum(sizes[p][q] for p in range(n)) for q in range(n)))
+            per_chunk.append(sizes)
+        recv, addrs = self._p2p_buffer(cap)
+        stream = torch.cuda.current_stream(self.device)
+        for k in range(K):
+            sizes = per_chunk[k]
+            entries = []
             for q in range(n):
-                base = sum(pc.numel for p in range(self.gpu)
-                           for pc in repartition_pieces(old_layouts[p], new_layouts[q]))
-                for pc in repartition_pieces(old_layouts[self.gpu], new_layouts[q]):
-                    p2p_entries.append((pc.src_off * 2, addrs[q] + base * 2, pc.src_ld * 2, pc.cols * 2, pc.rows,
-                                        pc.cols * 2))
-                    base += pc.numel
-            pd, ptot = _copy_desc_rows(p2p_entries)
-            stream = torch.cuda.current_stream(self.device)
+                if q == me:
+                    continue
+                base = sum(sizes[p][q] for p in range(me))
+                for pc in pieces[me][q]:
+                    sl = pc.row_slice(k, K)
+                    if sl is not None:
+                        entries.append((sl.src_off * 2, addrs[q] + base * 2, sl.src_ld * 2, sl.cols * 2, sl.rows,
+                                        sl.cols * 2))
+                        base += sl.numel
+            _, recv_e, _, _ = self._weight_chunk(pieces, k, K)
             stream.synchronize()
-            self.replica_comm.barrier()  # every receive buffer exists and is idle
-            if ptot:
+            self.replica_comm.barrier()  # every receive buffer is idle (previous chunk unpacked)
+            if entries:
+                pd, ptot = _copy_desc_rows(entries)
                 ops.copy2d_batched(old.arena, None, torch.from_numpy(pd).to(self.device), ptot)
             stream.synchronize()
-            self.replica_comm.barrier()  # every piece landed
-        else:
-            send = torch.empty(max(s_pos, 8), dtype=torch.bfloat16, device=self.device)
-            sd, stot = _copy_desc_rows(send_entries)
-            if stot:
-                ops.copy2d_batched(old.arena, send, torch.from_numpy(sd).to(self.device), stot)
-            self.replica_comm.all_to_all(recv, send, recv_splits, send_splits)
-        if rtot:
-            ops.copy2d_batched(recv, new.arena, torch.from_numpy(rd).to(self.device), rtot)
-        self.state = new
-        return 2 * (s_pos - send_splits[self.gpu])
+            self.replica_comm.barrier()  # every piece of chunk k landed
+            if recv_e:
+                rd, rtot = _copy_desc_rows(recv_e)
+                ops.copy2d_batched(recv, new.arena, torch.from_numpy(rd).to(self.device), rtot)
 
     # ---------------------------------------------------------- KV reshard --
     def reshard_kv(self, cfg_new: ParallelismConfig, block_ids: np.ndarray, chunk_blocks: int = 256) -> int:
@@ -329,9 +468,7 @@ class Worker:
         # transfer.  Chunks are disjoint block sets, so packing chunk i+1 from
         # the old layout while unpacking chunk i into the new one is safe.
         main = torch.cuda.current_stream(self.device)
-        if getattr(self, "_comm_stream", None) is None:
-            self._comm_stream = torch.cuda.Stream(self.device)
-        cs = self._comm_stream
+        cs = self._comm_stream_()
         arrived: list = [None] * len(chunks)
 
         def launch(i):
@@ -368,11 +505,7 @@ class Worker:
         chunk = min(chunk_blocks, ids_all.size)
         # identical on every rank: the buffer every rank allocates and maps
         recv_cells = max(sum(r.cells for r in e.recv) for e in ex)
-        key = (src_cfg, dst_cfg, chunk, recv_cells)
-        if getattr(self, "_p2p", None) is None or self._p2p[0] != key:
-            recv = torch.empty(chunk * recv_cells * cell + 8, dtype=torch.bfloat16, device=self.device)
-            self._p2p = (key, recv, self.replica_comm.peer_addresses(recv))
-        _, recv, addrs = self._p2p
+        recv, addrs = self._p2p_buffer(chunk_blocks * recv_cells * cell + 8)
         stream = torch.cuda.current_stream(self.device)
         sent = 0
         for c0 in range(0, ids_all.size, chunk):
@@ -594,6 +727,13 @@ class Worker:
         n = h_last.shape[0]
         vals = torch.empty(n, dtype=torch.float32, device=self.device)
         idxs = torch.empty(n, dtype=torch.int32, device=self.device)
+        ar = self._arena(n) if st.tp_comm.size > 1 and not self.record_logits and self.fuse_argmax else None
+        if ar is not None:
+            # every rank's argmax keys meet over peer memory: no all-gather
+            ops.lm_head_keys(h_last, self.w("head"), st.weights.vocab_begin, ar.keys[:n], workspace=ws,
+                             rownorm=rownorm)
+            ar.argmax(n, out_tokens)
+            return
         if self.record_logits or not self.fuse_argmax:
             logits = ops.gemm(h_last, self.w("head"), out_f32=True, workspace=ws, rownorm=rownorm)
             ops.argmax_rows(logits, st.weights.vocab_begin, vals, idxs)
@@ -675,6 +815,113 @@ class Worker:
         h_last = ops.rmsnorm(x, self.w("final_norm"), a.rms_eps, row_idx=last)
         self._logits_argmax(h_last, first_tokens)
 
+    def decode_round(self, tokens: torch.Tensor, ctx_lens: torch.Tensor, tables: torch.Tensor,
+                     positions: torch.Tensor, slots: torch.Tensor, out_tokens: torch.Tensor,
+                     spans: list[tuple[int, int]]) -> None:
+        """One decode round of the batch: every row advances one token.
+
+        pp = 1: one decode step of the whole batch (``spans`` is one span).
+        pp > 1 (sim.py:517-535): the rows are split into the micro-batches
+        ``spans`` (ceil(n/pp) rows each); every stage runs its layers on each
+        micro-batch in turn — stage 0 embeds, the others receive the
+        activations from the previous stage, the last stage computes the
+        greedy tokens — so micro-batch i+1 enters stage 0 while micro-batch
+        i is in stage 1 (the pipeline).  At the end of the round the last
+        stage returns the round's tokens to stage 0, which embeds them next
+        round (the pipeline drains once per round)."""
+        st = self.state
+        if st.cfg.pp == 1:
+            assert len(spans) == 1 and spans[0] == (0, tokens.numel())
+            self.decode_step(tokens, ctx_lens, tables, positions, slots, out_tokens)
+            return
+        a = self.arch
+        geo = self.geometry()
+        nq, nk = st.weights.n_q_heads, st.weights.n_kv_heads
+        first, last = st.stage == 0, st.stage == st.cfg.pp - 1
+        for lane, (b0, b1) in enumerate(spans):
+            n = b1 - b0
+            buf = self._buffers(n, lane=lane)
+            v = dict(tok=tokens[b0:b1], ctx=ctx_lens[b0:b1], tab=tables[b0:b1], pos=positions[b0:b1],
+                     slot=slots[b0:b1], out=out_tokens[b0:b1])
+            ops.decode_positions(v["ctx"], v["tab"], self.block_size, v["pos"], v["slot"])
+            ar = self._arena(n)
+            h_ready = False
+            if ar is not None:
+                x = ar.x[:n]
+            else:
+                x = buf.get("x")
+                if x is None or x.shape[0] != n:
+                    x = buf["x"] = torch.empty(n, a.hidden, dtype=torch.bfloat16, device=self.device)
+            if first:
+                if ar is not None:
+                    ops.embedding(v["tok"], self.w("embed"), st.weights.vocab_begin, ar.part[:n])
+                    ar.combine(n, self.w(f"L{st.weights.layer_begin}.attn_norm"), a.rms_eps)
+                    h_ready = True
+                else:
+                    ops.embedding(v["tok"], self.w("embed"), st.weights.vocab_begin, x)
+                    if st.tp_comm.size > 1:
+                        st.tp_comm.all_reduce_(x)
+            else:
+                self.replica_comm.recv(x, st.pp_prev)
+
+            def attn(qkv, layer_local, v=v, buf=buf):
+                return ops.decode_attention(qkv, nq, nk, self.pool, geo.as_tuple(), self.num_blocks,
+                                            layer_local, v["tab"], v["ctx"], buf["attn"], self.scale)
+
+            for layer in self._layers():
+                h_ready = self._block(x, layer, attn, buf, (v["pos"], v["slot"]), ar=ar, h_ready=h_ready,
+                                      final=last)
+            if not last:
+                self.replica_comm.send(x, st.pp_next)
+                continue
+            rn = None
+            if ar is not None and h_ready:
+                h = ar.h[:n]
+            elif self.fold_norm and st.tp_comm.size == 1 and h_ready:
+                h, rn = x, self._final_rownorm(buf, n, int(h_ready))
+            else:
+                h = ops.rmsnorm(x, self.w("final_norm"), a.rms_eps, out=buf["h"])
+            self._logits_argmax(h, v["out"], buf["ws"], rownorm=rn)
+        # the round's tokens back to the stage that embeds them
+        src = (st.cfg.pp - 1) * st.cfg.tp + st.rank
+        dst = st.rank
+        if last:
+            self.replica_comm.send(out_tokens, dst)
+        elif first:
+            self.replica_comm.recv(out_tokens, src)
+
+    def runtime_reserve_bytes(self, cfg_p: ParallelismConfig, cfg_d: ParallelismConfig, max_prefill_tokens: int) -> int:
+        """HBM this GPU needs beyond its weights and KV pool at the peak of a
+        run (ADVICE: the pool must leave room for it):
+          * a weight re-partition holds the new arena next to the old one,
+            plus two chunk buffers each way (SSB_RESHARD_CHUNK_MB);
+          * the KV re-shard stages 256 blocks of its rectangles twice each way;
+          * prefill activations of a max_prefill_tokens forward (h, x, qkv,
+            attention out, gate/up product, row sums) and the fp32 logits of
+            its last rows; decode buffers are smaller;
+          * GEMM split-K workspaces, the fused-TP peer arena, host-tier
+            staging, and 2 GiB of allocator slack."""
+        a = self.arch
+        mx = 0
+        cfgs = {cfg_p, cfg_d}
+        if len(cfgs) > 1:
+            new = max(weight_layout(a, c.tp, c.pp, self.gpu).arena_elems for c in cfgs) * 2
+            mx = new + 4 * self.RESHARD_CHUNK_BYTES
+            blk = max(kv_geometry(a, c.tp, c.pp, 1, self.block_size).block_elems for c in cfgs) * 2
+            mx = max(mx, 4 * 256 * blk)
+        T = max_prefill_tokens
+        tp = min(c.tp for c in cfgs)
+        act = T * (2 * a.hidden + a.qkv_dim // tp + a.num_query_heads * a.head_dim // tp + a.ffn // tp) * 2
+        act += 2 * T * (-(-a.hidden // 64)) * 4 + 2 * T * 4 * (a.vocab // tp) // max(T // 512, 1)
+        ws = 2 * self.GEMM_WS_BYTES + 3 * T * a.hidden * 2
+        return int(mx + act + ws + (2 << 30))
+
+    def check_peer_errors(self) -> None:
+        """Raise if a fused TP combine's peer barrier timed out (host sync)."""
+        for ar in self._tp_arenas.values():
+            if ar.usable:
+                ar.check()
+
     def decode_step(self, tokens: torch.Tensor, ctx_lens: torch.Tensor, tables: torch.Tensor,
                     positions: torch.Tensor, slots: torch.Tensor, out_tokens: torch.Tensor) -> None:
         """One decode step of the resident batch under a pure-TP layout:
@@ -687,11 +934,101 @@ class Worker:
         B = tokens.numel()
         lanes = self.decode_lanes if (B >= 2 * self.min_lane_rows and not self.record_logits) else 1
         if lanes == 1:
+            if self._graph_ok(B):
+                self._decode_step_graph(tokens, ctx_lens, tables, positions, slots, out_tokens)
+                return
             self._decode_lanes([(0, B)], tokens, ctx_lens, tables, positions, slots, out_tokens, 0)
             return
         h = B // 2
         self._decode_lanes([(0, h), (h, B)], tokens, ctx_lens, tables, positions, slots, out_tokens,
                            self.lane_gemm_cap)
+
+    # ------------------------------------------------------- CUDA graphs --
+    def _graph_ok(self, B: int) -> bool:
+        """A decode step is captured in a CUDA graph when nothing in it needs
+        the host: one lane, a pure tensor-parallel layout whose collectives
+        all run as peer-memory kernels (the fused combine and the peer argmax;
+        tp = 1 has none), no logit recording, no per-launch profiling."""
+        from . import _lib
+
+        if not self.cuda_graphs or self.device.type != "cuda" or self.record_logits or _lib.STATS.timing:
+            return False
+        st = self.state
+        if st.cfg.pp != 1:
+            return False
+        if st.tp_comm.size > 1:
+            return self.fuse_argmax and self._arena(B) is not None
+        return True
+
+    def _decode_step_graph(self, tokens, ctx_lens, tables, positions, slots, out_tokens) -> None:
+        """Replay the captured decode step of this batch size: the step's
+        inputs are copied into the graph's static buffers, its outputs copied
+        back.  A batch size is captured the second time it occurs (the first
+        occurrence runs eagerly and warms every lazy allocation); the ~6L+10
+        library launches of a step become one graph launch, which removes the
+        per-launch host cost that bounds a TP8 step (~2-3 ms of GPU work)."""
+        from . import _lib
+
+        B = tokens.numel()
+        st = self.state
+        ar = self._arena(B) if st.tp_comm.size > 1 else None
+        key = (B, tables.shape[1], st.cfg, self.pool.data_ptr(), st.arena.data_ptr(),
+               ar.generation if ar is not None else 0, self.fold_norm,
+               self.fuse_rope, self.split_k)
+        ent = self._graphs.get(key)
+        if ent is None:
+            ent = self._graphs[key] = {
+                "tok": torch.empty_like(tokens), "ctx": torch.empty_like(ctx_lens), "tab": torch.empty_like(tables),
+                "pos": torch.empty_like(positions), "slot": torch.empty_like(slots),
+                "out": torch.empty_like(out_tokens), "graph": None, "seen": 0, "launches": 0}
+        ent["tok"].copy_(tokens)
+        ent["ctx"].copy_(ctx_lens)
+        ent["tab"].copy_(tables)
+        args = (ent["tok"], ent["ctx"], ent["tab"], ent["pos"], ent["slot"], ent["out"])
+        if ent["graph"] is not None:
+            ent["graph"].replay()
+            _lib.STATS.count += ent["launches"]
+        else:
+            self._decode_lanes([(0, B)], *args, 0)
+            ent["seen"] += 1
+            if ent["seen"] >= 2:
+                self._capture(ent, args, B)
+        ctx_lens.copy_(ent["ctx"])
+        positions.copy_(ent["pos"])
+        slots.copy_(ent["slot"])
+        out_tokens.copy_(ent["out"])
+
+    def _capture(self, ent: dict, args, B: int) -> None:
+        """Record one decode step on the static buffers into a CUDA graph
+        (capture only records; the step that just ran eagerly was the real
+        one).  A capture failure disables graphs for this worker."""
+        from . import _lib
+
+        if self._graph_pool is None:
+            self._graph_pool = torch.cuda.graph_pool_handle()
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(self.device)
+        cap.wait_stream(torch.cuda.current_stream(self.device))
+        n0 = _lib.STATS.count
+        try:
+            with torch.cuda.graph(g, pool=self._graph_pool, stream=cap, capture_error_mode="thread_local"):
+                self._decode_lanes([(0, B)], *args, 0)
+        except RuntimeError as exc:  # noqa: BLE001 - any capture failure falls back to eager launches
+            import warnings
+
+            warnings.warn(f"decode-step CUDA graph capture failed ({exc}); running eagerly", RuntimeWarning,
+                          stacklevel=2)
+            self.cuda_graphs = False
+            _lib.STATS.count = n0
+            return
+        torch.cuda.current_stream(self.device).wait_stream(cap)
+        ent["launches"] = _lib.STATS.count - n0
+        _lib.STATS.count = n0
+        ent["graph"] = g
+
+    def _drop_graphs(self) -> None:
+        """Forget every captured step (weights, pool or peer arena moved)."""
+        self._graphs.clear()
 
     def _decode_lanes(self, spans, tokens, ctx_lens, tables, positions, slots, out_tokens, cap) -> None:
         st = self.state

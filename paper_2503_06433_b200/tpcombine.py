@@ -24,11 +24,17 @@ import warnings
 import torch
 
 from . import ops
+from ._lib import SeesawKernelError
 from .comm import Comm
+
+
+_GENERATION = [0]
 
 
 class PeerArena:
     def __init__(self, comm: Comm, device: torch.device, hidden: int, rows: int, max_blocks: int) -> None:
+        _GENERATION[0] += 1
+        self.generation = _GENERATION[0]   # distinguishes arenas whose id() was reused (graph cache keys)
         self.comm = comm
         self.hidden = hidden
         self.rows = rows
@@ -38,23 +44,43 @@ class PeerArena:
         self.x = torch.zeros(rows, hidden, dtype=bf, device=device)
         self.h = torch.zeros(rows, hidden, dtype=bf, device=device)
         self.sig = torch.zeros(ops.tp_signal_bytes() // 4, dtype=torch.int32, device=device)
+        # the LM head's argmax keys of every row (vocab-parallel greedy token)
+        self.keys = torch.zeros(rows, dtype=torch.int64, device=device)
         self.err = torch.zeros(1, dtype=torch.int32, device=device)
         torch.cuda.current_stream(device).synchronize()
-        self.addrs = {k: comm.peer_addresses(getattr(self, k)) for k in ("part", "x", "h", "sig")}
-        self.epoch = 0
+        self._maps: list = []  # peer mappings live exactly as long as the arena
+        self.addrs = {k: comm.peer_addresses(getattr(self, k), self._maps)
+                      for k in ("part", "x", "h", "sig", "keys")}
         self.usable = self._self_test()
 
-    def combine(self, rows: int, gamma: torch.Tensor | None, eps: float, err: bool = False) -> None:
-        """x[:rows], h[:rows] (if gamma) <- sum over ranks of part[:rows]."""
-        self.epoch += 1
+    def combine(self, rows: int, gamma: torch.Tensor | None, eps: float) -> None:
+        """x[:rows], h[:rows] (if gamma) <- sum over ranks of part[:rows].
+        A peer that misses the device barrier for 30 s sets the error word
+        (checked by :meth:`check` at the engine's synchronisation points)
+        instead of trapping the context.  The barrier epochs live on the
+        device (epoch 0), so the call may be captured in a CUDA graph."""
         a = self.addrs
         ops.tp_allreduce_rmsnorm(a["part"], a["x"], a["h"] if gamma is not None else None, a["sig"],
-                                 self.comm.rank, rows, self.hidden, gamma, eps, self.epoch, self.max_blocks,
-                                 self.err if err else None)
+                                 self.comm.rank, rows, self.hidden, gamma, eps, 0, self.max_blocks, self.err)
+
+    def argmax(self, rows: int, out_idx: torch.Tensor) -> None:
+        """out_idx[:rows] <- greedy token of every row from the ranks' LM-head
+        keys (keys[:rows], written by ops.lm_head_keys)."""
+        ops.tp_argmax_keys(self.addrs["keys"], self.addrs["sig"], self.comm.rank, rows, out_idx, 0,
+                           self.max_blocks, self.err)
+
+    def check(self) -> None:
+        """Raise if any combine since the last check timed out (host sync)."""
+        code = int(self.err.item())
+        if code:
+            self.err.zero_()
+            raise SeesawKernelError(f"fused TP combine: peer barrier timed out (error word {code}) on rank "
+                                        f"{self.comm.rank}; the TP group's peers stopped participating")
 
     def _self_test(self) -> bool:
         """Known answer: rank r's part = (r + 1) * ramp; x must be the exact
-        bf16 of the fp32 sum, and h its rmsnorm (gamma = 1)."""
+        bf16 of the fp32 sum, and h its rmsnorm (gamma = 1); the argmax of
+        synthetic keys must pick every row's largest key."""
         n, r = self.comm.size, self.comm.rank
         rows = min(self.rows, 64)
         dev = self.part.device
@@ -65,9 +91,21 @@ class PeerArena:
             want += (ramp * (p + 1) / 64).to(torch.bfloat16).float()
         want = want.to(torch.bfloat16)
         gamma = torch.ones(self.hidden, dtype=torch.bfloat16, device=dev)
-        self.combine(rows, gamma, 1e-5, err=True)
+        self.combine(rows, gamma, 1e-5)
         ref_h = ops.rmsnorm(want, gamma, 1e-5)
-        ok = (int(self.err.item()) == 0 and torch.equal(self.x[:rows], want) and torch.equal(self.h[:rows], ref_h))
+        # argmax keys: rank p's key of row i = ((3i + 5p) % 7) << 32 | ~(100p + i)
+        i = torch.arange(rows, device=dev, dtype=torch.int64)
+
+        def key(p):
+            return (((3 * i + 5 * p) % 7) << 32) | (0xFFFFFFFF - (100 * p + i))
+
+        self.keys[:rows].copy_(key(r))
+        best = torch.stack([key(p) for p in range(n)]).amax(0)
+        want_idx = (0xFFFFFFFF - (best & 0xFFFFFFFF)).to(torch.int32)
+        got_idx = torch.empty(rows, dtype=torch.int32, device=dev)
+        self.argmax(rows, got_idx)
+        ok = (int(self.err.item()) == 0 and torch.equal(self.x[:rows], want) and torch.equal(self.h[:rows], ref_h)
+              and torch.equal(got_idx, want_idx))
         flags = torch.tensor([1.0 if ok else 0.0], device=dev)
         self.comm.all_reduce_(flags)  # every member agrees on the outcome
         good = int(flags.item()) == n

@@ -32,6 +32,8 @@ def oracle_arch(a) -> lo.Arch:
 
 
 def run_threads(n, fn, timeout=900):
+    """Run fn(rank) on n threads; the first failure is re-raised (the other
+    ranks' ThreadComm waits time out instead of hanging)."""
     out, errs = [None] * n, []
 
     def body(r):
@@ -49,18 +51,36 @@ def run_threads(n, fn, timeout=900):
         t.join(timeout=timeout)
     if errs:
         raise errs[0]
+    if any(t.is_alive() for t in ts):
+        raise TimeoutError(f"rank threads still running after {timeout} s")
+    return out
+
+
+def step_logits(worker) -> dict:
+    """{(request id, step): fp32 logits} of a run with record_logits: step 0
+    is the prefill's last position, step k the k-th decode step's input
+    position (the engine logs each recorded forward's row ids)."""
+    out, count = {}, {}
+    assert len(worker.logit_rows) == len(worker.logit_log)
+    for rec, ids in zip(worker.logit_log, worker.logit_rows):
+        assert rec.shape[0] == len(ids)
+        for j, sid in enumerate(ids):
+            k = count.get(sid, 0)
+            count[sid] = k + 1
+            out[(sid, k)] = rec[j]
     return out
 
 
 def greedy_margins(arch, reqs, prompts, outputs, tp_prefill, tp_decode, max_pos=256, pp_prefill=1,
-                   fold_norm=True, weights=None):
+                   fold_norm=True, weights=None, gpu_logits=None, pp_decode=1):
     """Teacher-forced comparison with the bf16-faithful oracle: per step
-    (seq, step, gpu token, oracle token, oracle top-1/top-2 margin).
-    ``fold_norm`` mirrors the engine default (SSB_FOLD_NORM=1) on the
-    tensor-parallel-1 phases; ``pp_prefill`` places the stage boundaries."""
+    (seq, step, gpu token, oracle token, oracle top-1/top-2 margin, measured
+    max |gpu - oracle| logit deviation or None).  ``fold_norm`` mirrors the
+    engine default (SSB_FOLD_NORM=1) on the tensor-parallel-1 phases;
+    ``pp_prefill`` places the stage boundaries."""
     oracle = lo.LlamaOracle(oracle_arch(arch), seed=0, bf16_faithful=True, max_pos=max_pos,
                             tp_prefill=tp_prefill, tp_decode=tp_decode, fold_norm=fold_norm, pp_prefill=pp_prefill,
-                            weights=weights)
+                            weights=weights, pp_decode=pp_decode)
     rows = []
     for r, p in zip(reqs, prompts):
         got = outputs[r.id]
@@ -68,40 +88,42 @@ def greedy_margins(arch, reqs, prompts, outputs, tp_prefill, tp_decode, max_pos=
         exp, logs = oracle.generate(p, r.output_len, forced=got)
         for k, (g, e, lg) in enumerate(zip(got, exp, logs)):
             top2 = torch.topk(lg, 2).values
-            rows.append((r.id, k, g, e, float(top2[0] - top2[1])))
+            dev = None if gpu_logits is None else (gpu_logits[(r.id, k)] - lg).abs().max().item()
+            rows.append((r.id, k, g, e, float(top2[0] - top2[1]), dev))
     return rows
 
 
 # Greedy identity.  The GPU and the bf16-faithful oracle round to bf16 at the
 # same points but accumulate in fp32 in different orders (tensor-core MMA vs
 # einsum), which flips a few bf16 roundings per step and moves the logits by
-# ~1e-3.  Two tokens whose oracle logits are closer than that are a tie at
-# the computation's precision.  A substitution is therefore accepted only
-# when the oracle's top-1/top-2 margin is below TIE_EPS (or, where the test
-# recorded the GPU's logits, below the measured GPU-vs-oracle deviation of
-# that very step), and every substitution is counted and reported.
-TIE_EPS = 4e-3
+# ~0.02 (measured: median 0.018 on configs[0]).  Two tokens whose oracle
+# logits are closer than the GPU's deviation on that step are a tie at the
+# computation's precision.  A substitution is therefore accepted only when
+# the oracle's top-1/top-2 margin is below the GPU-vs-oracle logit deviation
+# MEASURED on that very step (tests that record the GPU's logits), else
+# below TIE_EPS; every substitution is counted and reported, and at most 1 %
+# of the steps may have one.
+TIE_EPS = 0.02
 
 
 def check_greedy(arch, reqs, prompts, outputs, tp_prefill, tp_decode, max_pos=256, pp_prefill=1,
-                 fold_norm=True, deviations=None, max_subs=None, weights=None):
+                 fold_norm=True, gpu_logits=None, max_subs=None, weights=None, pp_decode=1):
     """Greedy identity against the bf16-faithful oracle (teacher forced).
-    ``deviations``: {(seq id, step): max |gpu - oracle| logit deviation}
-    measured by the caller; a substitution at a step with a known deviation
-    must have margin <= that deviation, otherwise margin < TIE_EPS.
-    Returns {"steps", "substitutions": [(seq, step, gpu, oracle, margin)],
-    "min_margin"}."""
+    ``gpu_logits``: step_logits() of the run.  Returns {"steps",
+    "substitutions": [(seq, step, gpu, oracle, margin, deviation)],
+    "min_margin", "deviations"}."""
     rows = greedy_margins(arch, reqs, prompts, outputs, tp_prefill, tp_decode, max_pos, pp_prefill, fold_norm,
-                          weights)
+                          weights, gpu_logits, pp_decode)
     subs = [r for r in rows if r[2] != r[3]]
-    for sid, k, g, e, margin in subs:
-        bound = TIE_EPS if deviations is None else deviations[(sid, k)]
+    for sid, k, g, e, margin, dev in subs:
+        bound = TIE_EPS if dev is None else dev
         assert margin <= bound, (f"seq {sid} step {k}: gpu {g} != oracle {e} with oracle margin {margin:.5f} "
                                  f"> {bound:.5f}")
     limit = max(1, len(rows) // 100) if max_subs is None else max_subs
     assert len(subs) <= limit, f"{len(subs)} near-tie substitutions in {len(rows)} steps: {subs}"
     margins = np.array([r[4] for r in rows])
-    return {"steps": len(rows), "substitutions": subs, "min_margin": float(margins.min())}
+    devs = np.array([r[5] for r in rows if r[5] is not None])
+    return {"steps": len(rows), "substitutions": subs, "min_margin": float(margins.min()), "deviations": devs}
 
 
 def _owned(arch, tp: int, pp: int, gpu: int) -> dict[str, tuple[int, int, int, int]]:

@@ -177,6 +177,70 @@ def sim_golden() -> dict:
     return {"runs": out}
 
 
+def _fleet(model: ModelSpec, gpu_seqs: float, cpu_seqs: float, seq_tokens: int, num_gpus: int = 1,
+           dp: int = 1) -> HardwareSpec:
+    """The reference tests' sim_fleet (pkg/tests/conftest.py:88-110): each
+    replica's GPU tier holds exactly gpu_seqs sequences of seq_tokens, the
+    shared CPU tier cpu_seqs."""
+    k = seq_tokens * kv_bytes_per_token(model)
+    return HardwareSpec(num_gpus=num_gpus, hbm_bandwidth=1e12, peak_flops=1e14,
+                        gpu_memory=(total_weight_bytes(model) + gpu_seqs * k) * dp / num_gpus,
+                        host_memory_per_gpu=max(cpu_seqs, 1e-9) * k / num_gpus, host_link_bandwidth=1.6e10,
+                        allreduce=RingAllReduce(1.6e10))
+
+
+# BASELINE configs[0]'s tiny LLaMA (2 layers, hidden 256, 4 heads, d=64, ffn
+# 768, vocab 1024) as the reference ModelSpec: params_per_layer folded as
+# total/L (paper_2503_06433_b200.arch.LlamaArch.model_spec)
+TINY = ModelSpec(num_layers=2, params_per_layer=1114752, num_query_heads=4, num_kv_heads=4, head_dim=64)
+
+
+def _event_rows(rep) -> list:
+    """The schedule of a run without its clock: (kind, seq, replica, payload
+    fields that describe the schedule)."""
+    rows = []
+    for e in rep.event_log:
+        p = e.payload
+        keep = {k: (list(v) if isinstance(v, tuple) else v) for k, v in p.items()
+                if k in ("phase", "index", "direction", "seqs", "batch", "tokens")}
+        rows.append([e.kind, e.seq_id, e.gpu_id, keep])
+    return rows
+
+
+def schedule_golden() -> dict:
+    """Reference simulate() schedules on the tiny LLaMA that the real engine
+    reproduces (tests/test_schedule_gpu.py): the [4,4] two-cycle case
+    (test_sim.py:79-101), the transition law (test_sim.py:103-117), the
+    decode- and prefill-prioritized policies, pipeline decode (ceil(n/pp)
+    micro-batches) and DP replicas."""
+    out = []
+    lens8 = [(24, 8), (24, 3), (24, 5), (24, 2), (24, 7), (24, 4), (24, 6), (24, 1)]
+    cases = [
+        # name, policy, p, d, n_gpus, dp, gpu_seqs, cpu_seqs, seq_tokens, lens, force_mixed
+        ("tm_4_4", "transition-min", (1, 1, 1), (1, 1, 1), 1, 1, 2, 4, 32, [(24, 8)] * 8, False),
+        ("tm_pp2_tp2", "transition-min", (1, 2, 1), (2, 1, 1), 2, 1, 2, 4, 32, [(24, 8)] * 8, False),
+        ("decode_prio", "decode", (1, 1, 1), (1, 1, 1), 1, 1, 3, 0, 32, lens8, False),
+        ("decode_prio_pp2", "decode", (1, 2, 1), (1, 2, 1), 2, 1, 5, 0, 32, lens8, False),
+        ("decode_prio_dp2", "decode", (1, 1, 2), (1, 1, 2), 2, 2, 2, 0, 32, lens8, False),
+        ("prefill_prio", "prefill", (1, 1, 1), (1, 1, 1), 1, 1, 3, 0, 32, lens8, False),
+        ("prefill_prio_mixed", "prefill", (1, 2, 1), (2, 1, 1), 2, 1, 3, 0, 32, lens8, True),
+    ]
+    for n, cpu, gpu in [(8, 3, 1), (5, 2, 2), (7, 7, 3), (1, 1, 1), (10, 4, 2), (6, 1, 3)]:
+        cases.append((f"law_{n}_{cpu}_{gpu}", "transition-min", (1, 1, 1), (1, 1, 1), 1, 1, gpu, cpu, 19,
+                      [(16, 3)] * n, False))
+    for name, pol, p, d, ng, dp, gs, cs, toks, lens, mixed in cases:
+        hw = _fleet(TINY, gs, cs, toks, num_gpus=ng, dp=dp)
+        reqs = [Request(i, a, b) for i, (a, b) in enumerate(lens)]
+        rep = simulate(TINY, hw, reqs, SchedulingPolicy(pol), ParallelismConfig(*p), ParallelismConfig(*d),
+                       SimOptions(force_mixed=mixed))
+        out.append({"name": name, "policy": pol, "p": list(p), "d": list(d), "num_gpus": ng,
+                    "gpu_memory": hw.gpu_memory, "host_memory_per_gpu": hw.host_memory_per_gpu,
+                    "host_link_bandwidth": hw.host_link_bandwidth, "lens": [list(x) for x in lens],
+                    "force_mixed": mixed, "transitions": rep.transitions, "replay_ok": bool(replay_check(rep)),
+                    "events": _event_rows(rep)})
+    return {"model": model_doc(TINY), "runs": out}
+
+
 def perf_golden() -> dict:
     """Reference cost-model values (perf.py) the restated model must equal."""
     from shardsim import perf
@@ -206,6 +270,7 @@ def main() -> None:
     (OUT / "perf.json").write_text(json.dumps(perf_golden(), sort_keys=True))
     (OUT / "planning.json").write_text(json.dumps(planning_golden(), sort_keys=True))
     (OUT / "simulate.json").write_text(json.dumps(sim_golden(), sort_keys=True))
+    (OUT / "schedule.json").write_text(json.dumps(schedule_golden(), sort_keys=True))
     print("wrote", OUT / "planning.json", OUT / "simulate.json", "with shardsim", shardsim.__version__)
 
 

@@ -25,7 +25,7 @@ import numpy as np
 import pytest
 import torch
 
-from engine_helpers import check_greedy, oracle_arch, oracle_weights_from_worker, tiny_hw
+from engine_helpers import check_greedy, oracle_arch, oracle_weights_from_worker, step_logits, tiny_hw
 from oracle import llama as lo
 from paper_2503_06433_b200 import PRESETS, execute, replay_check
 from paper_2503_06433_b200.comm import SoloComm
@@ -52,31 +52,25 @@ def default_path(cuda):
     model = arch.model_spec()
     fused = execute(model, hw, reqs, SchedulingPolicy.TRANSITION_MINIMIZING, cfg, cfg, arch=arch, prompts=prompts,
                     comm=SoloComm(), device=dev, worker=wk)
-    wk.logit_log = []
+    wk.logit_log, wk.logit_rows = [], []
     recorded = execute(model, hw, reqs, SchedulingPolicy.TRANSITION_MINIMIZING, cfg, cfg, arch=arch,
                        prompts=prompts, comm=SoloComm(), device=dev, worker=wk, record_logits=True)
     logs = [x.clone() for x in wk.logit_log]
+    gpu_logits = step_logits(wk)
     weights = oracle_weights_from_worker(wk, arch)
-    return arch, reqs, prompts, fused, recorded, logs, weights
+    return arch, reqs, prompts, fused, recorded, logs, weights, gpu_logits
 
 
 def test_default_path_greedy_tokens(default_path):
     """Tokens of the fused default path vs the bf16-faithful oracle; a
     substitution only where the oracle margin is below the GPU-vs-oracle
     logit deviation measured on that step (recorded run, same tokens)."""
-    arch, reqs, prompts, fused, recorded, logs, weights = default_path
+    arch, reqs, prompts, fused, recorded, logs, weights, gpu_logits = default_path
     assert replay_check(fused)
     assert recorded.outputs == fused.outputs
-    orc = lo.LlamaOracle(oracle_arch(arch), seed=0, bf16_faithful=True, max_pos=512, weights=weights,
-                         fold_norm=True)
-    dev = {}
-    for i, (r, p) in enumerate(zip(reqs, prompts)):
-        _, ref = orc.generate(p, r.output_len, forced=fused.outputs[r.id])
-        for k, (g, e) in enumerate(zip(_rows(logs, reqs, i, r), ref)):
-            dev[(r.id, k)] = (g - e).abs().max().item()
-    stats = check_greedy(arch, reqs, prompts, fused.outputs, 1, 1, max_pos=512, deviations=dev, weights=weights,
-                         max_subs=1)
-    d = np.array(list(dev.values()))
+    stats = check_greedy(arch, reqs, prompts, fused.outputs, 1, 1, max_pos=512, gpu_logits=gpu_logits,
+                         weights=weights, max_subs=1)
+    d = stats["deviations"]
     print(f"default path (8B shape, 2 layers): {stats['steps']} steps, substitutions {stats['substitutions']}, "
           f"smallest margin {stats['min_margin']:.5f}, deviation median {np.median(d):.5f} max {d.max():.5f}")
 
@@ -93,7 +87,7 @@ def _rows(logs, reqs, i, r):
 
 
 def test_default_path_logits_within_bf16_tolerance(default_path):
-    arch, reqs, prompts, fused, recorded, logs, weights = default_path
+    arch, reqs, prompts, fused, recorded, logs, weights, _ = default_path
     # the argmax epilogue picks the argmax of the logits the unfused head writes
     assert recorded.outputs == fused.outputs
     orc = lo.LlamaOracle(oracle_arch(arch), seed=0, bf16_faithful=False, max_pos=512, weights=weights)

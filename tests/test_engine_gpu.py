@@ -27,7 +27,7 @@ from paper_2503_06433_b200.report import SchedulingPolicy
 from paper_2503_06433_b200.runtime import Worker
 from paper_2503_06433_b200.specs import ParallelismConfig, Request
 
-from engine_helpers import check_greedy, oracle_arch, run_threads, tiny_hw  # noqa: F401 (re-exported)
+from engine_helpers import check_greedy, oracle_arch, run_threads, step_logits, tiny_hw  # noqa: F401
 
 pytestmark = pytest.mark.gpu
 
@@ -151,20 +151,10 @@ def test_greedy_tokens_match_oracle(tiny_run):
     deviation distribution are printed for the record."""
     arch, reqs, prompts, res, _ = tiny_run
     rep, wk = res[1]  # rank 1 = last PP stage: prefill and decode logits
-    logs = wk.logit_log
-    n = len(reqs)
-    prefill, decode = torch.cat(logs[:n]), logs[n:]
-    orc = lo.LlamaOracle(oracle_arch(arch), seed=0, bf16_faithful=True, max_pos=256, tp_prefill=1, tp_decode=2,
-                         fold_norm=True, pp_prefill=2)
-    dev = {}
-    for i, (r, p) in enumerate(zip(reqs, prompts)):
-        _, ref = orc.generate(p, r.output_len, forced=rep.outputs[r.id])
-        got = [prefill[i]] + [decode[k][i] for k in range(r.output_len - 1)]
-        for k, (g, e) in enumerate(zip(got, ref)):
-            dev[(r.id, k)] = (g - e).abs().max().item()
-    stats = check_greedy(arch, reqs, prompts, rep.outputs, 1, 2, pp_prefill=2, deviations=dev)
+    stats = check_greedy(arch, reqs, prompts, rep.outputs, 1, 2, pp_prefill=2, gpu_logits=step_logits(wk))
     assert stats["steps"] == sum(r.output_len for r in reqs) == 256
-    d = np.array(list(dev.values()))
+    d = stats["deviations"]
+    assert d.size == 256
     print(f"configs[0]: {stats['steps']} greedy steps, {len(stats['substitutions'])} near-tie substitutions "
           f"{stats['substitutions']}; smallest oracle margin {stats['min_margin']:.5f}; GPU-vs-oracle logit "
           f"deviation median {np.median(d):.5f} p99 {np.quantile(d, 0.99):.5f} max {d.max():.5f}")
@@ -216,7 +206,7 @@ def test_host_tier_event_log(tiered_run):
 
 def test_host_tier_greedy_tokens(tiered_run):
     arch, reqs, prompts, res, _ = tiered_run
-    check_greedy(arch, reqs, prompts, res[0][0].outputs, 1, 2, pp_prefill=2)
+    check_greedy(arch, reqs, prompts, res[0][0].outputs, 1, 2, pp_prefill=2, gpu_logits=step_logits(res[1][1]))
 
 
 def test_host_tier_single_gpu(cuda):
@@ -224,7 +214,7 @@ def test_host_tier_single_gpu(cuda):
                                             gpu_seqs=2, n_req=6)
     rep = res[0][0]
     assert rep.config["host_tier"] and replay_check(rep)
-    check_greedy(arch, reqs, prompts, rep.outputs, 1, 1)
+    check_greedy(arch, reqs, prompts, rep.outputs, 1, 1, gpu_logits=step_logits(res[0][1]))
 
 
 def _run_ragged(arch_name, cfg_p, cfg_d, lens, gpu_seqs=None, gpu_memory=2e9, record_logits=False, fused_tp=False,
@@ -258,7 +248,7 @@ def _run_ragged(arch_name, cfg_p, cfg_d, lens, gpu_seqs=None, gpu_memory=2e9, re
             torch.cuda.current_stream(dev).synchronize()
             if fused_tp:
                 assert wk._tp_arenas and all(a.usable for a in wk._tp_arenas.values())
-        return (rep, [x.clone() for x in wk.logit_log]) if record_logits else rep
+        return (rep, [x.clone() for x in wk.logit_log], step_logits(wk)) if record_logits else rep
 
     return arch, reqs, prompts, run_threads(W, body)
 
@@ -273,13 +263,13 @@ def test_ragged_lengths_pp2_to_tp2(cuda, gpu_seqs):
     decode steps (the batch shrinks and the GEMM plans change shape), with and
     without the host tier; tokens match the oracle, the log replays."""
     arch, reqs, prompts, res = _run_ragged("tiny", ParallelismConfig(1, 2, 1), ParallelismConfig(2, 1, 1), RAGGED,
-                                           gpu_seqs=gpu_seqs)
-    rep = res[0]
+                                           gpu_seqs=gpu_seqs, record_logits=True)
+    rep = res[0][0]
     assert replay_check(rep), replay_check(rep).violation
-    assert rep.outputs == res[1].outputs
+    assert rep.outputs == res[1][0].outputs
     if gpu_seqs is not None:
         assert rep.config["host_tier"]
-    check_greedy(arch, reqs, prompts, rep.outputs, 1, 2, pp_prefill=2)
+    check_greedy(arch, reqs, prompts, rep.outputs, 1, 2, pp_prefill=2, gpu_logits=res[1][2])
 
 
 def test_ragged_lengths_llama_shape_single_gpu(cuda):
@@ -301,7 +291,7 @@ def test_ragged_lengths_llama_shape_single_gpu(cuda):
                                    gpu_memory=20e9, record_logits=True)
     finally:
         PRESETS.pop("llama3-8b-2l", None)
-    (rep1, logs1), (rep2, _), (_, logs2) = one[0], two[0], two[1]
+    (rep1, logs1, _), (rep2, _, _), (_, logs2, _) = one[0], two[0], two[1]
     assert replay_check(rep1) and replay_check(rep2) and rep2.transitions == 1
     pre1 = logs1[0]                          # [10, V]: one packed forward
     pre2 = torch.cat(logs2[: len(reqs)])     # one micro-batch per prompt on the last stage
@@ -365,7 +355,7 @@ def test_fused_tp_combine_bit_identical(cuda, arch_name, cfg_p, cfg_d):
     finally:
         if arch_name != "tiny":
             PRESETS.pop(arch_name, None)
-    (rb, lb), (rf, lf) = base[0], fused[0]
+    (rb, lb, _), (rf, lf, _) = base[0], fused[0]
     assert replay_check(rf), replay_check(rf).violation
     assert rf.outputs == rb.outputs
     assert len(lb) == len(lf) and all(torch.equal(a, b) for a, b in zip(lb, lf))
@@ -391,7 +381,7 @@ def test_folded_norm_matches_rmsnorm_path(cuda, arch_name):
     finally:
         if arch_name != "tiny":
             PRESETS.pop(arch_name, None)
-    (rb, lb), (rf, lf) = base[0], fold[0]
+    (rb, lb, _), (rf, lf, gl) = base[0], fold[0]
     assert replay_check(rf), replay_check(rf).violation
     assert len(lb) == len(lf)
     # record 0 = the packed prefill of every prompt (rows in request order);
@@ -417,4 +407,5 @@ def test_folded_norm_matches_rmsnorm_path(cuda, arch_name):
     # every request's prefill row plus at least half of all decode rows
     assert rows_compared >= len(reqs) + sum(r.output_len for r in reqs) // 2, (rows_compared, flipped)
     if arch_name == "tiny":
-        check_greedy(PRESETS[arch_name], reqs, synthetic_prompts(reqs, PRESETS[arch_name].vocab), rf.outputs, 1, 1)
+        check_greedy(PRESETS[arch_name], reqs, synthetic_prompts(reqs, PRESETS[arch_name].vocab), rf.outputs, 1, 1,
+                     gpu_logits=gl)

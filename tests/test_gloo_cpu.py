@@ -89,7 +89,10 @@ def _rank(rank, port, outdir):
     _emulate_ops(runtime.ops)
     arch = PRESETS["tiny"]
     w = runtime.Worker(arch, TorchComm(), 1, torch.device("cpu"), seed=0, max_pos=64)
+    # stream the weight re-partition in many chunks (the 8B/70B regime)
+    w.RESHARD_CHUNK_BYTES = 200_000
     w.init_weights(ParallelismConfig(TP_P, PP_P, 1))
+    np.save(f"{outdir}/arena_p_{rank}.npy", w.state.arena.view(torch.int16).numpy().copy())
     w.alloc_pool(NB)
     rng = np.random.default_rng(100 + rank)
     w.pool.view(torch.int16).copy_(torch.from_numpy(rng.integers(-3000, 3000, w.pool.numel(), dtype=np.int16)))
@@ -98,8 +101,13 @@ def _rank(rank, port, outdir):
     sent_w = w.repartition_weights(ParallelismConfig(TP_D, PP_D, 1))
     np.save(f"{outdir}/pool_after_{rank}.npy", w.pool.view(torch.int16).numpy().copy())
     np.save(f"{outdir}/arena_{rank}.npy", w.state.arena.view(torch.int16).numpy().copy())
+    chunks = w._weight_plan(ParallelismConfig(TP_P, PP_P, 1), ParallelismConfig(TP_D, PP_D, 1))[1]
+    # and back: TP2 -> PP2 (the norm gains are replicated on both TP ranks;
+    # only rank 0 of a stage sends them)
+    sent_back = w.repartition_weights(ParallelismConfig(TP_P, PP_P, 1))
+    np.save(f"{outdir}/arena_back_{rank}.npy", w.state.arena.view(torch.int16).numpy().copy())
     with open(f"{outdir}/sent_{rank}.txt", "w") as fh:
-        fh.write(f"{sent_kv} {sent_w}")
+        fh.write(f"{sent_kv} {sent_w} {sent_back} {chunks}")
     dist.destroy_process_group()
 
 
@@ -113,7 +121,8 @@ def _free_port() -> int:
 def gloo_run():
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(_rank, args=(_free_port(), d), nprocs=2, join=True)
-        out = {k: [np.load(f"{d}/{k}_{r}.npy") for r in range(2)] for k in ("pool_before", "pool_after", "arena")}
+        out = {k: [np.load(f"{d}/{k}_{r}.npy") for r in range(2)]
+               for k in ("pool_before", "pool_after", "arena", "arena_p", "arena_back")}
         out["sent"] = [tuple(map(int, open(f"{d}/sent_{r}.txt").read().split())) for r in range(2)]
     return out
 
@@ -151,3 +160,24 @@ def test_weight_repartition_two_processes_bit_exact(gloo_run):
                 bits = (full.view(np.uint32) >> 16).astype(np.uint16).view(np.int16)
                 np.testing.assert_array_equal(loc[s.dst_row : s.dst_row + s.rows, s.dst_col : s.dst_col + s.cols],
                                               bits[s.row0 : s.row0 + s.rows, s.col0 : s.col0 + s.cols])
+
+
+def test_weight_repartition_streams_in_chunks_and_round_trips(gloo_run):
+    """The P->D re-partition ran in many chunks; D->P restores the prefill
+    arenas bit for bit, and each element crossed once (the replicated norm
+    gains are sent by tensor rank 0 only)."""
+    from paper_2503_06433_b200 import PRESETS
+
+    a = PRESETS["tiny"]
+    for r in range(2):
+        np.testing.assert_array_equal(gloo_run["arena_back"][r], gloo_run["arena_p"][r])
+    sent_kv, sent_w, sent_back, chunks = zip(*gloo_run["sent"])
+    assert min(chunks) > 4
+    # TP2 -> PP2 on the 2-layer model: GPU 0 (TP rank 0) sends stage 1 its
+    # half of layer 1's matrices and of the LM head, plus layer 1's two norm
+    # gains and the final norm (it is its stage's rank 0); GPU 1 sends
+    # stage 0 its half of layer 0's matrices and of the embedding, no gains
+    h, f, v = a.hidden, a.ffn, a.vocab
+    matrices = h * a.qkv_dim + a.num_query_heads * a.head_dim * h + 3 * h * f
+    half = matrices // 2 + v * h // 2
+    assert sent_back == (2 * (half + 3 * h), 2 * half)

@@ -30,6 +30,7 @@ import torch
 
 from engine_helpers import (
     check_greedy,
+    step_logits,
     expected_kv_bytes_per_token_sent,
     expected_weight_bytes_sent,
     oracle_arch,
@@ -52,7 +53,7 @@ L8 = LlamaArch("l8-d128", 8, 512, 16, 8, 128, 1024, 2048, rope_theta=500000.0)
 BS = 64
 
 
-def _run(arch, cfg_p, cfg_d, reqs, prompts, gpu_memory=4e9, fused_tp=False, snap_weights=None):
+def _run(arch, cfg_p, cfg_d, reqs, prompts, gpu_memory=4e9, fused_tp=False, snap_weights=None, record_logits=False):
     """``snap_weights``: ranks whose post-transition arena is copied to the
     host (None: all)."""
     W = cfg_p.num_gpus
@@ -79,11 +80,11 @@ def _run(arch, cfg_p, cfg_d, reqs, prompts, gpu_memory=4e9, fused_tp=False, snap
 
             wk.hooks = {"before_reshard": before, "after_reshard": after}
             rep = execute(model, hw, reqs, SchedulingPolicy.TRANSITION_MINIMIZING, cfg_p, cfg_d, arch=arch,
-                          prompts=prompts, comm=comms[r], device=dev, worker=wk)
+                          prompts=prompts, comm=comms[r], device=dev, worker=wk, record_logits=record_logits)
             torch.cuda.current_stream(dev).synchronize()
             if fused_tp:
                 assert wk._tp_arenas and all(a.usable for a in wk._tp_arenas.values())
-            return rep, wk.replica, wk.gpu
+            return rep, wk.replica, wk.gpu, (step_logits(wk) if record_logits else None)
 
     return run_threads(W, body), snaps
 
@@ -151,21 +152,21 @@ def pp8_tp8(cuda):
     reqs = [Request(i, a, b) for i, (a, b) in enumerate(LENS)]
     prompts = synthetic_prompts(reqs, L8.vocab)
     cfg_p, cfg_d = ParallelismConfig(1, 8, 1), ParallelismConfig(8, 1, 1)
-    res, snaps = _run(L8, cfg_p, cfg_d, reqs, prompts)
+    res, snaps = _run(L8, cfg_p, cfg_d, reqs, prompts, record_logits=True)
     return reqs, prompts, cfg_p, cfg_d, res, snaps
 
 
 def test_pp8_tp8_replay_and_schedule(pp8_tp8):
     reqs, _, _, _, res, _ = pp8_tp8
-    for rep, replica, _ in res:
+    for rep, replica, _, _ in res:
         assert replica == 0
         assert replay_check(rep), replay_check(rep).violation
         assert rep.transitions == 1
         assert rep.config["cfg_p"] == "tp1.pp8.dp1" and rep.config["cfg_d"] == "tp8.pp1.dp1"
     # every rank saw the same schedule (SPMD) and the same tokens
-    logs = [[(e.kind, e.seq_id) for e in rep.event_log] for rep, _, _ in res]
+    logs = [[(e.kind, e.seq_id) for e in rep.event_log] for rep, _, _, _ in res]
     assert all(lg == logs[0] for lg in logs)
-    assert all(rep.outputs == res[0][0].outputs for rep, _, _ in res)
+    assert all(rep.outputs == res[0][0].outputs for rep, _, _, _ in res)
 
 
 def test_pp8_tp8_weights_bit_exact(pp8_tp8):
@@ -176,13 +177,13 @@ def test_pp8_tp8_kv_bit_exact_and_bytes(pp8_tp8):
     reqs, _, cfg_p, cfg_d, res, snaps = pp8_tp8
     blocks = _check_pools(L8, snaps, range(8), cfg_p, cfg_d)
     assert blocks.size == sum(-(-(a + b) // BS) for a, b in LENS)
-    for rep, _, gpu in res:
+    for rep, _, gpu, _ in res:
         _check_bytes(L8, rep, gpu, cfg_p, cfg_d, blocks.size)
 
 
 def test_pp8_tp8_greedy_tokens(pp8_tp8):
     reqs, prompts, _, _, res, _ = pp8_tp8
-    check_greedy(L8, reqs, prompts, res[0][0].outputs, 1, 8, max_pos=512, pp_prefill=8)
+    check_greedy(L8, reqs, prompts, res[0][0].outputs, 1, 8, max_pos=512, pp_prefill=8, gpu_logits=res[7][3])
 
 
 @pytest.fixture(scope="module")
@@ -191,13 +192,13 @@ def pp4_tp4_dp2(cuda):
     reqs = [Request(i, a, b) for i, (a, b) in enumerate(lens)]
     prompts = synthetic_prompts(reqs, L8.vocab)
     cfg_p, cfg_d = ParallelismConfig(1, 4, 2), ParallelismConfig(4, 1, 2)
-    res, snaps = _run(L8, cfg_p, cfg_d, reqs, prompts)
+    res, snaps = _run(L8, cfg_p, cfg_d, reqs, prompts, record_logits=True)
     return reqs, prompts, cfg_p, cfg_d, res, snaps
 
 
 def test_dp2_replicas_split_round_robin(pp4_tp4_dp2):
     reqs, _, _, _, res, _ = pp4_tp4_dp2
-    for rank, (rep, replica, gpu) in enumerate(res):
+    for rank, (rep, replica, gpu, _) in enumerate(res):
         assert (replica, gpu) == divmod(rank, 4)
         assert replay_check(rep), replay_check(rep).violation
         assert rep.transitions == 1
@@ -206,7 +207,7 @@ def test_dp2_replicas_split_round_robin(pp4_tp4_dp2):
         # the event log covers every replica (gpu_id = replica index, sim.py:101)
         gpus = {e.gpu_id for e in rep.event_log if e.kind == "prefill_complete"}
         assert gpus == {0, 1}
-    logs = [[(e.kind, e.seq_id, e.gpu_id) for e in rep.event_log] for rep, _, _ in res]
+    logs = [[(e.kind, e.seq_id, e.gpu_id) for e in rep.event_log] for rep, _, _, _ in res]
     assert all(lg == logs[0] for lg in logs)
 
 
@@ -217,7 +218,7 @@ def test_dp2_weights_and_kv_bit_exact(pp4_tp4_dp2):
         ranks = range(4 * replica, 4 * replica + 4)
         blocks = _check_pools(L8, snaps, ranks, cfg_p, cfg_d)
         for r in ranks:
-            rep, _, gpu = res[r]
+            rep, _, gpu, _ = res[r]
             _check_bytes(L8, rep, gpu, cfg_p, cfg_d, blocks.size)
 
 
@@ -226,7 +227,8 @@ def test_dp2_greedy_tokens(pp4_tp4_dp2):
     for replica in range(2):
         mine = [(r, p) for i, (r, p) in enumerate(zip(reqs, prompts)) if i % 2 == replica]
         out = res[4 * replica][0].outputs
-        check_greedy(L8, [r for r, _ in mine], [p for _, p in mine], out, 1, 4, max_pos=512, pp_prefill=4)
+        check_greedy(L8, [r for r, _ in mine], [p for _, p in mine], out, 1, 4, max_pos=512, pp_prefill=4,
+                     gpu_logits=res[4 * replica + 3][3])
 
 
 def test_pp8_tp8_fused_combine_same_tokens(pp8_tp8):
@@ -249,12 +251,12 @@ def test_llama3_8b_pp8_tp8_volumes(cuda):
     prompts = synthetic_prompts(reqs, arch.vocab)
     cfg_p, cfg_d = ParallelismConfig(1, 8, 1), ParallelismConfig(8, 1, 1)
     res, snaps = _run(arch, cfg_p, cfg_d, reqs, prompts, gpu_memory=8e9, snap_weights=(0, 3, 7))
-    assert all(replay_check(rep) for rep, _, _ in res)
+    assert all(replay_check(rep) for rep, _, _, _ in res)
     blocks = _check_pools(arch, snaps, range(8), cfg_p, cfg_d)
     per_tok = [expected_kv_bytes_per_token_sent(arch, (1, 8), (8, 1), g) for g in range(8)]
     assert per_tok == [14336] * 8
     w = [res[g][0].measured["weight_bytes_sent"] for g in range(8)]
     assert abs(sum(w) / 8 - 1.757e9) < 1e6
-    for rep, _, gpu in res:
+    for rep, _, gpu, _ in res:
         _check_bytes(arch, rep, gpu, cfg_p, cfg_d, blocks.size)
     _check_weights(arch, snaps, [0, 3, 7], full_rows=False)

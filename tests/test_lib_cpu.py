@@ -72,12 +72,17 @@ def test_rownorm_and_tp_combine_argument_errors():
     rc = lib.ssb_gemm_bf16_rn(16, 16, 16, None, 128, 128, 64, 64, 64, 128, 0, 0, 0, 0, None, 0, ctypes.byref(rn),
                               None)
     assert rc < 0 and b"ss_in" in lib.ssb_last_error()
-    assert lib.ssb_tp_signal_bytes() == 2 * 512 * 8 * 4
+    # two barrier phases x 512 CTAs x 8 ranks, then 512 per-CTA epoch counters
+    assert lib.ssb_tp_signal_bytes() == (2 * 512 * 8 + 512) * 4
     addrs = _lib.uint64_array([16, 32])
-    rc = lib.ssb_tp_allreduce_rmsnorm(addrs, addrs, None, addrs, 2, 0, 4, 256, 256, None, 1e-5, 0, 4, None, None)
-    assert rc < 0 and b"epoch" in lib.ssb_last_error()
     rc = lib.ssb_tp_allreduce_rmsnorm(addrs, addrs, None, addrs, 9, 0, 4, 256, 256, None, 1e-5, 1, 4, None, None)
     assert rc < 0 and b"nranks" in lib.ssb_last_error()
+    rc = lib.ssb_tp_allreduce_rmsnorm(addrs, addrs, None, addrs, 2, 0, 4, 250, 256, None, 1e-5, 0, 4, None, None)
+    assert rc < 0 and b"hidden" in lib.ssb_last_error()
+    rc = lib.ssb_tp_argmax_keys(addrs, addrs, 2, 3, 4, None, 0, 4, None, None)
+    assert rc < 0 and b"rank" in lib.ssb_last_error()
+    rc = lib.ssb_tp_argmax_keys(addrs, addrs, 2, 0, 4, None, 0, 4, None, None)
+    assert rc < 0 and b"null" in lib.ssb_last_error()
 
 
 def test_tp_arena_cache_grows_collectively(monkeypatch):

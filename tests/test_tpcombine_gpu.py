@@ -15,6 +15,8 @@ from __future__ import annotations
 import pytest
 import torch
 
+from paper_2503_06433_b200._lib import SeesawKernelError
+
 from paper_2503_06433_b200 import ops
 from paper_2503_06433_b200.comm import ThreadComm
 from paper_2503_06433_b200.tpcombine import PeerArena
@@ -49,7 +51,7 @@ def test_combine_bit_exact(cuda, W, rows, hidden):
             outs = []
             for c in range(calls):
                 ar.part[:rows].copy_(parts[c])
-                ar.combine(rows, gamma if c % 2 == 0 else None, 1e-5, err=True)
+                ar.combine(rows, gamma if c % 2 == 0 else None, 1e-5)
                 outs.append((ar.x[:rows].clone(), ar.h[:rows].clone() if c % 2 == 0 else None))
             s.synchronize()
             assert int(ar.err.item()) == 0
@@ -83,9 +85,13 @@ def test_missing_peer_times_out_instead_of_hanging(cuda):
             ar = PeerArena(comms[r], dev, 256, 8, max_blocks=4)
             comms[r].barrier()
             if r == 0:
-                ar.combine(8, None, 1e-5, err=True)
+                ar.combine(8, None, 1e-5)
                 s.synchronize()
-                return int(ar.err.item())
+                code = int(ar.err.item())
+                with pytest.raises(SeesawKernelError, match="peer barrier timed out"):
+                    ar.check()
+                ar.check()  # the error word was consumed
+                return code
             return 0
 
     assert run_threads(2, body)[0] == 1
