@@ -644,14 +644,27 @@ class _Engine:
                           input_len=s.req.input_len, output_len=s.req.output_len)
                 self.running[r].append(s)
         tk_by_id = {id(s): tk for s, tk in tickets}
+        # reference mode: the whole wave fits the GPU tier, so (as in
+        # sim.py:403-429) every completion is logged before the swap-outs;
+        # native mode stages overflow through a small reserve, one sequence
+        # at a time, and logs each completion next to its swap-out
+        batched = self.tm_mode == "reference"
+        if batched:
+            for r in sorted(waves):
+                for s in waves[r]:
+                    if s.overflow:
+                        self.kv.gpu_used += s.kv_bytes
+                        self._log(t_end, "prefill_complete", seq=s.req.id, gpu=r, nbytes=s.kv_bytes,
+                                  input_len=s.req.input_len, output_len=s.req.output_len)
         for r in sorted(waves):
             for s in waves[r]:
                 if not s.overflow:
                     continue
-                mark = tk_by_id[id(s)].done if id(s) in tk_by_id else t_end
-                self.kv.gpu_used += s.kv_bytes
-                self._log(mark, "prefill_complete", seq=s.req.id, gpu=r, nbytes=s.kv_bytes,
-                          input_len=s.req.input_len, output_len=s.req.output_len)
+                mark = t_end if batched else (tk_by_id[id(s)].done if id(s) in tk_by_id else t_end)
+                if not batched:
+                    self.kv.gpu_used += s.kv_bytes
+                    self._log(mark, "prefill_complete", seq=s.req.id, gpu=r, nbytes=s.kv_bytes,
+                              input_len=s.req.input_len, output_len=s.req.output_len)
                 self.kv.gpu_used -= s.kv_bytes
                 self.kv.cpu_used += s.kv_bytes
                 self.kv.residency[s.req.id] = Residency.CPU
@@ -724,8 +737,13 @@ class _Engine:
             parts_tok.append(torch.cat(ft))
             self.rows.append((list(fresh), torch.cat(ft).clone()))
         self.d_tables = torch.from_numpy(tab).to(dev)
-        self.d_ctx = torch.cat(parts_ctx).contiguous()
-        self.d_tokens = torch.cat(parts_tok).contiguous()
+        if order:
+            self.d_ctx = torch.cat(parts_ctx).contiguous()
+            self.d_tokens = torch.cat(parts_tok).contiguous()
+        else:
+            # this replica drained while others still decode (dp > 1)
+            self.d_ctx = torch.zeros(0, dtype=torch.int32, device=dev)
+            self.d_tokens = torch.zeros(0, dtype=torch.int32, device=dev)
         self.batch = order
 
     def _prefetch(self, fill: bool) -> None:

@@ -693,31 +693,61 @@ class Worker:
         if self.state.tp_comm.size > 1:
             self.state.tp_comm.all_reduce_(x)
 
-    def _buffers(self, T: int, lane: int = 0) -> dict:
-        """Activation buffers of a T-row forward, one set per decode lane."""
+    def _alloc_buffers(self, T: int) -> dict:
         st = self.state
         a = self.arch
         nq, nk = st.weights.n_q_heads, st.weights.n_kv_heads
-        key = ("buf", T, st.cfg.tp)
+        dev = self.device
+        return {
+            "h": torch.empty(T, a.hidden, dtype=torch.bfloat16, device=dev),
+            "qkv": torch.empty(T, (nq + 2 * nk) * a.head_dim, dtype=torch.bfloat16, device=dev),
+            "attn": torch.empty(T, nq * a.head_dim, dtype=torch.bfloat16, device=dev),
+            "act": torch.empty(T, st.weights.ffn_local, dtype=torch.bfloat16, device=dev),
+            # folded-norm row sums of squares: [T][N tiles] of the o_proj
+            # and down_proj outputs (N tile >= 64 columns)
+            "ss": [torch.empty(T * ((a.hidden + 63) // 64), dtype=torch.float32, device=dev) for _ in range(2)],
+        }
+
+    def _buffers(self, T: int, lane=0) -> dict:
+        """Activation buffers of a T-row forward, one set per decode lane.
+        Lane "graph" is the set the captured decode steps own: allocated at
+        a capacity (the largest batch seen) and handed out as [:T] views, so
+        every graph keeps pointing at live memory; growing it drops the
+        graphs (``_graph_capacity``)."""
+        st = self.state
+        a = self.arch
         slot = self._bufs.setdefault(lane, {})
-        if slot.get("key") != key:
-            dev = self.device
-            slot["key"] = key
-            slot["buf"] = {
-                "h": torch.empty(T, a.hidden, dtype=torch.bfloat16, device=dev),
-                "qkv": torch.empty(T, (nq + 2 * nk) * a.head_dim, dtype=torch.bfloat16, device=dev),
-                "attn": torch.empty(T, nq * a.head_dim, dtype=torch.bfloat16, device=dev),
-                "act": torch.empty(T, st.weights.ffn_local, dtype=torch.bfloat16, device=dev),
-                # folded-norm row sums of squares: [T][N tiles] of the o_proj
-                # and down_proj outputs (N tile >= 64 columns)
-                "ss": [torch.empty(T * ((a.hidden + 63) // 64), dtype=torch.float32, device=dev) for _ in range(2)],
-            }
+        if lane == "graph":
+            full = slot["full"]
+            tiles = (a.hidden + 63) // 64
+            buf = {k: v[:T] for k, v in full.items() if k != "ss"}
+            buf["ss"] = [s[: T * tiles] for s in full["ss"]]
+        else:
+            key = ("buf", T, st.cfg.tp)
+            if slot.get("key") != key:
+                slot["key"] = key
+                slot["buf"] = self._alloc_buffers(T)
+            buf = slot["buf"]
         if "ws" not in slot:
             # split-K workspace of this lane's stream (zeroed once; the GEMM
             # leaves its tile counters zero), see ssb_gemm_bf16_ws
             slot["ws"] = torch.zeros(self.GEMM_WS_BYTES, dtype=torch.uint8, device=self.device)
-        slot["buf"]["ws"] = slot["ws"] if self.split_k else None
-        return slot["buf"]
+        buf["ws"] = slot["ws"] if self.split_k else None
+        return buf
+
+    def _graph_capacity(self, B: int) -> None:
+        """Make the graph-owned buffers hold B rows under the current layout;
+        a reallocation invalidates every captured step."""
+        st = self.state
+        slot = self._bufs.setdefault("graph", {})
+        key = (st.cfg.tp, st.weights.ffn_local, st.weights.n_q_heads, st.weights.n_kv_heads)
+        if slot.get("key") == key and slot.get("cap", 0) >= B:
+            return
+        self._drop_graphs()
+        cap = max(B, slot.get("cap", 0) if slot.get("key") == key else 0)
+        full = self._alloc_buffers(cap)
+        full["x"] = torch.empty(cap, self.arch.hidden, dtype=torch.bfloat16, device=self.device)
+        slot.update(key=key, cap=cap, full=full)
 
     def _logits_argmax(self, h_last: torch.Tensor, out_tokens: torch.Tensor, ws: torch.Tensor | None = None,
                        rownorm=None) -> None:
@@ -972,6 +1002,7 @@ class Worker:
         B = tokens.numel()
         st = self.state
         ar = self._arena(B) if st.tp_comm.size > 1 else None
+        self._graph_capacity(B)
         key = (B, tables.shape[1], st.cfg, self.pool.data_ptr(), st.arena.data_ptr(),
                ar.generation if ar is not None else 0, self.fold_norm,
                self.fuse_rope, self.split_k)
@@ -989,14 +1020,39 @@ class Worker:
             ent["graph"].replay()
             _lib.STATS.count += ent["launches"]
         else:
-            self._decode_lanes([(0, B)], *args, 0)
+            self._decode_lanes([(0, B)], *args, 0, buf_lane="graph")
             ent["seen"] += 1
             if ent["seen"] >= 2:
-                self._capture(ent, args, B)
+                self._capture_group(ent, args, B)
         ctx_lens.copy_(ent["ctx"])
         positions.copy_(ent["pos"])
         slots.copy_(ent["slot"])
         out_tokens.copy_(ent["out"])
+
+    def _capture_group(self, ent: dict, args, B: int) -> None:
+        """Capture this rank's step.  Virtual ranks (ThreadComm threads on one
+        device) capture one at a time between host barriers: torch's capture
+        entry synchronizes the whole device and empties the allocator cache,
+        which must not happen while a peer thread is capturing, or while a
+        peer's combine kernel is still waiting on this rank's next step.  The
+        group agrees on the outcome, so no rank replays a graph while another
+        runs eagerly-with-a-failed-capture (their kernel sequences would
+        still match, but a mixed group is not worth the doubt)."""
+        from .comm import ThreadComm
+
+        tp = self.state.tp_comm
+        if not isinstance(tp, ThreadComm) or tp.size == 1:
+            self._capture(ent, args, B)
+            return
+        for turn in range(tp.size):
+            tp.barrier()
+            if turn == tp.rank:
+                self._capture(ent, args, B)
+        flags = tp._exchange(ent["graph"] is not None)
+        tp._done()
+        if not all(flags):
+            ent["graph"] = None
+            self.cuda_graphs = False
 
     def _capture(self, ent: dict, args, B: int) -> None:
         """Record one decode step on the static buffers into a CUDA graph
@@ -1012,7 +1068,7 @@ class Worker:
         n0 = _lib.STATS.count
         try:
             with torch.cuda.graph(g, pool=self._graph_pool, stream=cap, capture_error_mode="thread_local"):
-                self._decode_lanes([(0, B)], *args, 0)
+                self._decode_lanes([(0, B)], *args, 0, buf_lane="graph")
         except RuntimeError as exc:  # noqa: BLE001 - any capture failure falls back to eager launches
             import warnings
 
@@ -1030,7 +1086,8 @@ class Worker:
         """Forget every captured step (weights, pool or peer arena moved)."""
         self._graphs.clear()
 
-    def _decode_lanes(self, spans, tokens, ctx_lens, tables, positions, slots, out_tokens, cap) -> None:
+    def _decode_lanes(self, spans, tokens, ctx_lens, tables, positions, slots, out_tokens, cap,
+                      buf_lane=None) -> None:
         st = self.state
         a = self.arch
         main = torch.cuda.current_stream(self.device)
@@ -1047,7 +1104,7 @@ class Worker:
         for li, ((b0, b1), s) in enumerate(zip(spans, streams)):
             with torch.cuda.stream(s):
                 n = b1 - b0
-                buf = self._buffers(n, lane=li)
+                buf = self._buffers(n, lane=li if buf_lane is None else buf_lane)
                 v = dict(tok=tokens[b0:b1], ctx=ctx_lens[b0:b1], tab=tables[b0:b1], pos=positions[b0:b1],
                          slot=slots[b0:b1], out=out_tokens[b0:b1], h_ready=False)
                 ops.decode_positions(v["ctx"], v["tab"], self.block_size, v["pos"], v["slot"])

@@ -71,6 +71,7 @@ class PeerArena:
 
     def check(self) -> None:
         """Raise if any combine since the last check timed out (host sync)."""
+        torch.cuda.current_stream(self.err.device).synchronize()
         code = int(self.err.item())
         if code:
             self.err.zero_()
@@ -104,6 +105,9 @@ class PeerArena:
         want_idx = (0xFFFFFFFF - (best & 0xFFFFFFFF)).to(torch.int32)
         got_idx = torch.empty(rows, dtype=torch.int32, device=dev)
         self.argmax(rows, got_idx)
+        # wait with the GIL released: virtual ranks (threads) must still be
+        # able to launch their half of the barrier while this one waits
+        torch.cuda.current_stream(dev).synchronize()
         ok = (int(self.err.item()) == 0 and torch.equal(self.x[:rows], want) and torch.equal(self.h[:rows], ref_h)
               and torch.equal(got_idx, want_idx))
         flags = torch.tensor([1.0 if ok else 0.0], device=dev)
