@@ -217,6 +217,7 @@ def run_ours(args) -> None:
     e2e_times, e2e_reports = timed(prompts_pinned, max(1, min(args.steps, 2)))
     # per-kernel shares inside one instrumented batch
     kern = profile_kernels(one, prompts_dev, arch, args, dev, comm, world)
+    ar_table = allreduce_table(worker, dev, world, arch)
 
     out_tokens = args.prompts * args.output_len
     mean_t = sum(times) / len(times)
@@ -277,6 +278,8 @@ def run_ours(args) -> None:
         "clocks": clocks,
         "decode_attention_hbm_frac": (da.get("gbs", 0) / peaks["hbm_gbs"]) if da else None,
     }
+    if ar_table is not None:
+        line["allreduce_table"] = ar_table
     if n == 1:
         line["reshard_micro"] = reshard_microbench(worker, arch, args, peaks)
     if not args.no_cpu_baseline:
@@ -286,6 +289,63 @@ def run_ours(args) -> None:
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def allreduce_table(worker, dev, world: int, arch, rows: int = 512, iters: int = 20) -> dict | None:
+    """Measured all-reduce bandwidth per TP degree for the reference's
+    AllReduceTable (specs.py:103-133: time = message bytes / bandwidth(tp),
+    non-increasing in tp), on a decode-step message (rows x hidden bf16):
+    NCCL all_reduce over ranks [0, d) for d = 2, 4, ... <= world, and the
+    fused peer-memory combine (all-reduce + rmsnorm, csrc/tp_allreduce.cu) on
+    the decode TP group.  Outside the timed region; device time, max over
+    ranks.  None at N = 1 or without NCCL."""
+    import torch
+    import torch.distributed as dist
+
+    if world < 2 or dist.get_backend() != "nccl":
+        return None
+    x = torch.zeros(rows, arch.hidden, dtype=torch.bfloat16, device=dev)
+    nbytes = x.numel() * 2
+
+    def device_time(fn) -> float:
+        for _ in range(5):
+            fn()
+        torch.cuda.synchronize(dev)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(iters):
+            fn()
+        e.record()
+        torch.cuda.synchronize(dev)
+        return s.elapsed_time(e) / iters / 1e3
+
+    def max_over_ranks(t: float) -> float:
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
+    out: dict = {"msg_bytes": nbytes, "rows": rows, "nccl_s": {}, "nccl_algbw": {}}
+    d = 2
+    while d <= world:
+        grp = dist.new_group(list(range(d)))
+        t = device_time(lambda: dist.all_reduce(x, group=grp)) if dist.get_rank() < d else 0.0
+        t = max_over_ranks(t)
+        out["nccl_s"][d] = t
+        out["nccl_algbw"][d] = nbytes / t
+        d *= 2
+    # the AllReduceTable contract: bandwidth non-increasing in tp
+    table, lo = {}, float("inf")
+    for k in sorted(out["nccl_algbw"]):
+        lo = min(lo, out["nccl_algbw"][k])
+        table[k] = lo
+    out["allreduce_table"] = table
+    ar = next((a for a in worker._tp_arenas.values() if a.usable and a.comm.size == world), None)
+    if ar is not None and ar.rows >= rows:
+        gamma = torch.ones(arch.hidden, dtype=torch.bfloat16, device=dev)
+        t = max_over_ranks(device_time(lambda: ar.combine(rows, gamma, arch.rms_eps)))
+        out["fused_combine"] = {"degree": world, "s": t, "algbw": nbytes / t,
+                                "note": "all-reduce + the next rmsnorm, one peer-memory kernel"}
+    return out
 
 
 def _gemm_prefill_traffic(arch, args):

@@ -1,74 +1,167 @@
-"""Calibrate the reference cost model (perf.py, restating shardsim's
-perf.py:59-236) to the measured B200.
+"""The reference cost model (perf.py, restating shardsim's perf.py:59-236) on
+the MEASURED B200, and the reference optimizer re-run on it (SURVEY.md §8(f)
+row 3).
 
-The reference predicts a batch from a HardwareSpec's `peak_flops` and
-`hbm_bandwidth`.  This fits the two so that its prefill and decode phase
-predictions reproduce a measured bench line (prefill is compute-bound in the
-model, decode memory-bound), writes the fitted spec in the reference's YAML
-schema, and reports the model error before and after.  The fitted spec is
-what the reference's own optimizer (best_static / best_mixed) should be given
-to choose cfg_p / cfg_d for this hardware.
+1. Physical HardwareSpec: `peak_flops` = the measured sustained bf16 dense
+   rate and `hbm_bandwidth` = the measured copy bandwidth
+   (MEASURED_PEAKS.json, driver-written); the all-reduce model is the
+   measured AllReduceTable when a multi-GPU bench line carries one
+   (bench.py `allreduce_table`), else a ring at the nominal NVLink rate.
+   Written in the reference's YAML schema (specs.py:136-175) -- nothing in
+   it is fitted.
+2. Model error against a measured bench line, per phase, with the prefill
+   compute split into its linear term and its attention term.  The
+   reference's attention FLOPs use a d^2 factor (perf.py:9-11,
+   b*h_q*s^2*d^2 in prefill) where causal attention does 2*b*h_q*s^2*d:
+   a factor d/2 = 64 at head_dim 128.  That term alone is reported
+   separately (and the prediction with the conventional count beside it),
+   so the error is attributed instead of absorbed into an unphysical peak.
+3. The reference optimizer (best_static / best_mixed, optimize.py:161-196,
+   imported from baseline/_ref when present) run on the physical spec for
+   the bench workload.
 
-    python tools/calibrate.py profiles/r01/bench_line_final.jsonl configs/b200_x8_calibrated.yaml
+    python tools/calibrate.py BENCH_LINE.json [SCALE_LINE.json] \\
+        [--yaml configs/b200_x8_measured.yaml] [--json profiles/r02/model_error.json]
 """
 
 from __future__ import annotations
 
+import argparse
 import dataclasses
 import json
 import sys
 from pathlib import Path
 
-sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
 
 from paper_2503_06433_b200 import PRESETS, ParallelismConfig  # noqa: E402
-from paper_2503_06433_b200.perf import predict_phases  # noqa: E402
-from paper_2503_06433_b200.specs import HardwareSpec, RingAllReduce  # noqa: E402
+from paper_2503_06433_b200.perf import Phase, compute_time, layer_time_batch, predict_phases  # noqa: E402
+from paper_2503_06433_b200.specs import AllReduceTable, HardwareSpec, RingAllReduce  # noqa: E402
+
+NOMINAL_NVLINK = 900e9  # per direction, B200 NVLink 5
+
+
+def _last_json(path: Path) -> dict:
+    return json.loads([ln for ln in path.read_text().splitlines() if ln.startswith("{")][-1])
+
+
+def physical_spec(peaks: dict, num_gpus: int, ar_line: dict | None) -> HardwareSpec:
+    if ar_line and ar_line.get("allreduce_table"):
+        allreduce = AllReduceTable({int(k): float(v) for k, v in ar_line["allreduce_table"].items()})
+    else:
+        allreduce = RingAllReduce(NOMINAL_NVLINK)
+    return HardwareSpec(num_gpus=num_gpus, hbm_bandwidth=peaks["hbm_gbs"] * 1e9,
+                        peak_flops=peaks["bf16_tflops_sustained"] * 1e12, gpu_memory=180e9,
+                        host_memory_per_gpu=256e9, host_link_bandwidth=50e9, allreduce=allreduce)
+
+
+def prefill_terms(model, hw, cfg, input_len: int, prompts: int) -> dict:
+    """Prefill compute seconds of the batch: linear, attention with the
+    reference's d^2 count, attention with the conventional causal count."""
+    lin, att = compute_time(model, hw, cfg, prompts, input_len, Phase.PREFILL)
+    L = model.num_layers
+    conv = 2.0 * prompts * model.num_query_heads * input_len ** 2 * model.head_dim / (hw.peak_flops * cfg.tp)
+    return {"linear_s": L * lin, "attention_d2_s": L * att, "attention_conventional_s": L * conv,
+            "d2_over_conventional": att / conv if conv else None}
+
+
+def yaml_text(hw: HardwareSpec, source: str) -> str:
+    if isinstance(hw.allreduce, AllReduceTable):
+        ar = "allreduce_model:\n  kind: map\n  bandwidths:\n" + "".join(
+            f"    {k}: {v:.4e}\n" for k, v in sorted(hw.allreduce.bandwidths.items()))
+    else:
+        ar = f"allreduce_model:\n  kind: ring\n  interconnect_bandwidth: {hw.allreduce.interconnect_bandwidth:.4e}\n"
+    return ("# B200 HardwareSpec in the reference schema (specs.py:136-175): PHYSICAL, measured values,\n"
+            f"# nothing fitted.  {source}\n"
+            f"num_gpus: {hw.num_gpus}\nhbm_bandwidth: {hw.hbm_bandwidth:.4e}\npeak_flops: {hw.peak_flops:.4e}\n"
+            f"gpu_memory: {hw.gpu_memory:.1f}\nhost_memory_per_gpu: {hw.host_memory_per_gpu:.1f}\n"
+            f"host_link_bandwidth: {hw.host_link_bandwidth:.1f}\n" + ar)
+
+
+def run_optimizer(hw: HardwareSpec, model, cfg: dict) -> dict:
+    """best_static / best_mixed of the UNMODIFIED reference on this spec."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "shardsim").exists():
+        return {"unavailable": "baseline/_ref (the reference install) is absent"}
+    sys.path.insert(0, str(ref))
+    import shardsim as ss  # noqa: PLC0415
+
+    if isinstance(hw.allreduce, AllReduceTable):
+        ar = ss.AllReduceTable(dict(hw.allreduce.bandwidths))
+    else:
+        ar = ss.RingAllReduce(hw.allreduce.interconnect_bandwidth)
+    rhw = ss.HardwareSpec(hw.num_gpus, hw.hbm_bandwidth, hw.peak_flops, hw.gpu_memory, hw.host_memory_per_gpu,
+                          hw.host_link_bandwidth, ar)
+    rmodel = ss.ModelSpec(model.num_layers, model.params_per_layer, model.num_query_heads, model.num_kv_heads,
+                          model.head_dim, model.bytes_per_param)
+    summary = ss.WorkloadSummary(input_len=cfg["input_len"], output_len=cfg["output_len"], count=cfg["prompts"])
+    out = {}
+    for name in ("best_static", "best_mixed"):
+        plan = getattr(ss, name)(rmodel, rhw, summary)
+        out[name] = {"cfg_p": plan.cfg_p.label(), "cfg_d": plan.cfg_d.label(),
+                     "predicted_inverse_throughput": plan.predicted_inverse_throughput}
+    return out
 
 
 def main() -> None:
-    line = json.loads([ln for ln in Path(sys.argv[1]).read_text().splitlines() if ln.startswith("{")][-1])
-    out = Path(sys.argv[2]) if len(sys.argv) > 2 else None
+    ap = argparse.ArgumentParser()
+    ap.add_argument("bench", type=Path, help="a measured bench line (N=1)")
+    ap.add_argument("scale", type=Path, nargs="?", help="a multi-GPU bench line carrying allreduce_table")
+    ap.add_argument("--peaks", type=Path, default=ROOT / "MEASURED_PEAKS.json")
+    ap.add_argument("--gpus", type=int, default=8)
+    ap.add_argument("--yaml", type=Path)
+    ap.add_argument("--json", type=Path)
+    args = ap.parse_args()
+    line = _last_json(args.bench)
+    ar_line = _last_json(args.scale).get("allreduce_table") if args.scale else None
+    peaks = json.loads(args.peaks.read_text())
     cfg = line["config"]
     arch = PRESETS[cfg["workload"].split()[0]]
     model = arch.model_spec()
     n = line["n_gpus"]
     cfg_p, cfg_d = ParallelismConfig(1, n, 1), ParallelismConfig(n, 1, 1)
     meas = line["phases_s"]
-    hw0 = HardwareSpec(num_gpus=n, hbm_bandwidth=6.65e12, peak_flops=1.4e15, gpu_memory=180e9,
-                       host_memory_per_gpu=256e9, host_link_bandwidth=50e9, allreduce=RingAllReduce(770e9))
-
-    def predict(hw):
-        return predict_phases(model, hw, cfg_p, cfg_d, cfg["input_len"], cfg["output_len"], cfg["prompts"])
-
-    before = predict(hw0)
-    # each phase scales inversely with the one resource the model says binds it;
-    # iterate because the roofline max can switch terms
-    hw = hw0
-    for _ in range(20):
-        p = predict(hw)
-        hw = dataclasses.replace(hw, peak_flops=hw.peak_flops * p["prefill_s"] / meas["prefill"],
-                                 hbm_bandwidth=hw.hbm_bandwidth * p["decode_s"] / meas["decode"])
-    after = predict(hw)
+    hw = physical_spec(peaks, n, None)
+    pred = predict_phases(model, hw, cfg_p, cfg_d, cfg["input_len"], cfg["output_len"], cfg["prompts"])
+    terms = prefill_terms(model, hw, cfg_p, cfg["input_len"], cfg["prompts"])
+    # the same prediction with the conventional attention FLOP count: scale
+    # the attention compute term by 1/(d/2) (roofline max per layer)
+    lt = layer_time_batch(model, hw, cfg_p, [cfg["input_len"]] * cfg["prompts"], Phase.PREFILL)
+    conv_ratio = 1.0 / terms["d2_over_conventional"]
+    conv_layer = max(lt.t_dm_linear, lt.t_comp_linear) + max(lt.t_dm_attn, lt.t_comp_attn * conv_ratio) + lt.t_comm
+    pred_conv = model.num_layers * conv_layer
     tok = cfg["prompts"] * cfg["output_len"]
     res = {
+        "workload": cfg["workload"],
+        "physical_spec": {"peak_flops": hw.peak_flops, "hbm_bandwidth": hw.hbm_bandwidth,
+                          "source": f"{args.peaks.name}: bf16_tflops_sustained, hbm_gbs"},
         "measured": {"prefill_s": meas["prefill"], "decode_s": meas["decode"], "tokens_per_s": line["value"]},
-        "reference_model_nominal": {**before, "tokens_per_s": tok / (before["prefill_s"] + before["decode_s"]),
-                                    "hw": {"peak_flops": hw0.peak_flops, "hbm_bandwidth": hw0.hbm_bandwidth}},
-        "reference_model_calibrated": {**after, "tokens_per_s": tok / (after["prefill_s"] + after["decode_s"]),
-                                       "hw": {"peak_flops": hw.peak_flops, "hbm_bandwidth": hw.hbm_bandwidth}},
+        "reference_model": {**pred, "tokens_per_s": tok / (pred["prefill_s"] + pred["decode_s"]),
+                            "prefill_error": pred["prefill_s"] / meas["prefill"] - 1,
+                            "decode_error": pred["decode_s"] / meas["decode"] - 1},
+        "prefill_compute_terms": terms,
+        "reference_model_conventional_attention": {
+            "prefill_s": pred_conv, "prefill_error": pred_conv / meas["prefill"] - 1,
+            "note": "same model with the attention term at 2*b*h_q*s^2*d (causal) instead of b*h_q*s^2*d^2"},
     }
-    print(json.dumps(res, indent=1))
-    if out:
-        out.write_text(
-            "# B200 HardwareSpec (reference schema, specs.py:136-175) CALIBRATED so that the reference cost\n"
-            "# model (perf.py) reproduces the measured prefill / decode phase times of\n"
-            f"# {sys.argv[1]} ({cfg['workload']}): effective, not nominal, peaks.\n"
-            f"# tools/calibrate.py; nominal-model error before calibration: prefill "
-            f"{before['prefill_s'] / meas['prefill'] - 1:+.0%}, decode {before['decode_s'] / meas['decode'] - 1:+.0%}.\n"
-            f"num_gpus: 8\nhbm_bandwidth: {hw.hbm_bandwidth:.4e}\npeak_flops: {hw.peak_flops:.4e}\n"
-            "gpu_memory: 180000000000.0\nhost_memory_per_gpu: 256000000000.0\nhost_link_bandwidth: 50000000000.0\n"
-            "allreduce_model:\n  kind: ring\n  interconnect_bandwidth: 770000000000.0\n")
+    spec8 = physical_spec(peaks, args.gpus, {"allreduce_table": ar_line.get("allreduce_table")} if ar_line else None)
+    res["allreduce"] = ({"measured_table": spec8.allreduce.bandwidths, "source": str(args.scale)}
+                        if isinstance(spec8.allreduce, AllReduceTable)
+                        else {"ring_nominal": NOMINAL_NVLINK, "note": "no multi-GPU line with allreduce_table yet"})
+    try:
+        res["optimizer"] = run_optimizer(spec8, model, cfg)
+    except Exception as exc:  # noqa: BLE001 - report, the spec is still written
+        res["optimizer"] = {"error": repr(exc)}
+    print(json.dumps(res, indent=1, default=str))
+    if args.json:
+        args.json.parent.mkdir(parents=True, exist_ok=True)
+        args.json.write_text(json.dumps(res, indent=1, default=str) + "\n")
+    if args.yaml:
+        src = f"tools/calibrate.py from {args.peaks.name} ({peaks.get('when', '?')})"
+        if ar_line:
+            src += f"; all-reduce table from {args.scale}"
+        args.yaml.write_text(yaml_text(spec8, src))
 
 
 if __name__ == "__main__":
