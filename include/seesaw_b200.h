@@ -46,6 +46,12 @@ extern "C" {
 const char* ssb_last_error(void);
 int ssb_version(void);
 int ssb_device_sm_count(void);
+/* Programmatic dependent launch of the library's GEMM / decode-attention
+ * launches on (1) or off (0); returns the previous setting.  Default: the
+ * SSB_PDL environment variable, else on.  Virtual ranks that share one GPU
+ * and meet in the fused TP combine's device barrier must turn it off (a
+ * rank's early-resident GEMM could hold the SMs its peer's producer needs). */
+int ssb_set_pdl(int on);
 
 /* ------------------------------------------------------------------------
  * Dense projections (bf16 tcgen05/TMEM GEMM fed by TMA).
@@ -72,6 +78,10 @@ int ssb_gemm_bf16(const void* A, const void* B, void* C, const void* R, int M, i
 /* With SSB_GEMM_SPLIT(n): split only the tiles of the last, partial wave of
  * the persistent schedule ("tail split"); full waves run whole tiles. */
 #define SSB_GEMM_TAIL (1 << 28)
+/* Stream-K: whole tiles while two or more rounds remain, then the last
+ * rounds' k-blocks split evenly over the persistent CTAs; shared tiles are
+ * reduced in k order by their last contributor (needs a workspace). */
+#define SSB_GEMM_STREAMK (1 << 29)
 
 /* The same GEMM with a split-K workspace.  With block_n = 0 the library picks
  * (CTA pairs or single CTAs, N tile, number of k-splits) from a cost model of
@@ -283,6 +293,16 @@ int ssb_tp_allreduce_rmsnorm(const uint64_t* part_addrs, const uint64_t* x_addrs
                              const uint64_t* sig_addrs, int nranks, int rank, int rows, int hidden, int ld,
                              const void* gamma, float eps, uint32_t epoch, int max_blocks, uint32_t* err,
                              void* stream);
+
+/* The same combine for the folded-norm layout: x[:rows] <- sum of the
+ * ranks' partials on every rank (as above), and instead of h the per-row
+ * fp32 sum of squares of the stored bf16 x -- the reduction rmsnorm uses --
+ * into every rank's ss[rows]; the consumer GEMMs apply 1/rms from it
+ * (ssb_rownorm with ss_in_parts = 1) with the gains folded into their
+ * weights.  Halves the bytes each rank stores over NVLink. */
+int ssb_tp_allreduce_rowss(const uint64_t* part_addrs, const uint64_t* x_addrs, const uint64_t* ss_addrs,
+                           const uint64_t* sig_addrs, int nranks, int rank, int rows, int hidden, int ld,
+                           uint32_t epoch, int max_blocks, uint32_t* err, void* stream);
 
 /* Vocab-parallel greedy token of every row across the TP group over peer
  * memory (replaces the (max, idx) all-gathers + ssb_argmax_combine the

@@ -151,7 +151,7 @@ class LlamaOracle:
 
     def __init__(self, a: Arch, seed: int, bf16_faithful: bool = True, max_pos: int = 4096,
                  weights: dict[str, torch.Tensor] | None = None, tp_prefill: int = 1, tp_decode: int = 1,
-                 fold_norm: bool = False, pp_prefill: int = 1, pp_decode: int = 1) -> None:
+                 fold_norm: bool = False, pp_prefill: int = 1, pp_decode: int = 1, tp_fold: bool = False) -> None:
         self.a = a
         self.bf = bf16_faithful
         self.W = weights if weights is not None else init_model(a, seed)
@@ -159,6 +159,7 @@ class LlamaOracle:
         self.tp_prefill, self.tp_decode = tp_prefill, tp_decode
         self.tp = tp_prefill
         self.fold_norm, self.pp_prefill, self.pp_decode = fold_norm, pp_prefill, pp_decode
+        self.tp_fold = tp_fold
         self._decoding = False
 
     def _r(self, x: torch.Tensor) -> torch.Tensor:
@@ -176,8 +177,15 @@ class LlamaOracle:
         x1, x2 = x[..., :half], x[..., half:]
         return self._r(torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], dim=-1))
 
+    def _tp_folded(self) -> bool:
+        """Decode under a pure TP layout with the fused combine and the
+        folded norm (runtime.Worker._block_fused_folded, SSB_TP_FOLD=1): every
+        norm of the step is a 1/rms row scale of its consumer, the first
+        layer's too (the embedding's combine already leaves the row sums)."""
+        return self.fold_norm and self.tp_fold and self._decoding and self.tp > 1 and self.pp_decode == 1
+
     def _folding(self) -> bool:
-        return self.fold_norm and self.tp == 1
+        return self.fold_norm and (self.tp == 1 or self._tp_folded())
 
     def _inv_rms(self, x: torch.Tensor) -> torch.Tensor:
         return 1.0 / torch.sqrt((x * x).mean(-1, keepdim=True) + self.a.rms_eps)
@@ -197,7 +205,7 @@ class LlamaOracle:
         a, W, p = self.a, self.W, f"L{l}."
         d, hq, hk = a.head_dim, a.num_query_heads, a.num_kv_heads
         per_stage = a.num_layers // (self.pp_decode if self._decoding else self.pp_prefill)
-        fold_attn = self._folding() and l % per_stage != 0
+        fold_attn = self._folding() and (l % per_stage != 0 or self._tp_folded())
         q, k, v = self._normed_matmuls(x, W[p + "attn_norm"], [W[p + "wq"], W[p + "wk"], W[p + "wv"]], fold_attn)
         q = self._r(q).view(-1, hq, d)
         k = self._r(k).view(-1, hk, d)

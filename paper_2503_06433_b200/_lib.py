@@ -22,6 +22,7 @@ SSB_GEMM_MC2 = 1 << 17
 SSB_GEMM_2SM = 1 << 18
 SSB_GEMM_SPLIT_SHIFT = 20
 SSB_GEMM_TAIL = 1 << 28
+SSB_GEMM_STREAMK = 1 << 29
 SSB_MAX_PEERS = 64
 
 
@@ -98,6 +99,7 @@ SIGNATURES: dict[str, list] = {
     "ssb_decode_attention": [_P, _I, _I, _I, _P, KVGeometry, _I, _I, _P, _I, _P, _I, _P, _I, _F, _P],
     "ssb_tp_allreduce_rmsnorm": [_PU64, _PU64, _PU64, _PU64, _I, _I, _I, _I, _I, _P, _F, ctypes.c_uint32, _I, _P,
                                  _P],
+    "ssb_tp_allreduce_rowss": [_PU64, _PU64, _PU64, _PU64, _I, _I, _I, _I, _I, ctypes.c_uint32, _I, _P, _P],
     "ssb_tp_argmax_keys": [_PU64, _PU64, _I, _I, _I, _P, ctypes.c_uint32, _I, _P, _P],
 }
 
@@ -121,6 +123,8 @@ def load() -> ctypes.CDLL:
             lib.ssb_last_error.argtypes = []
             lib.ssb_version.restype = ctypes.c_int
             lib.ssb_device_sm_count.restype = ctypes.c_int
+            lib.ssb_set_pdl.restype = ctypes.c_int
+            lib.ssb_set_pdl.argtypes = [_I]
             lib.ssb_gemm_plan.restype = ctypes.c_int64
             lib.ssb_gemm_plan.argtypes = [_I, _I, _I, _I, _I, _I64, _PI32]
             lib.ssb_tp_signal_bytes.restype = ctypes.c_size_t

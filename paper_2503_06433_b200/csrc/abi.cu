@@ -2,6 +2,8 @@
 // cached device attributes and the driver entry point for TMA descriptors.
 #include <cudaTypedefs.h>
 
+#include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -38,6 +40,18 @@ int num_sms() {
     cache[dev] = n > 0 ? n : 148;
   }
   return cache[dev];
+}
+
+static std::atomic<int> g_pdl{-1};
+
+bool pdl_enabled() {
+  int v = g_pdl.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* e = getenv("SSB_PDL");
+    v = (e && atoi(e) == 0) ? 0 : 1;
+    g_pdl.store(v, std::memory_order_relaxed);
+  }
+  return v != 0;
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point, so the
@@ -85,6 +99,12 @@ const char* ssb_last_error(void) { return ssb::g_err; }
 int ssb_version(void) { return SSB_ABI_VERSION; }
 
 int ssb_device_sm_count(void) { return ssb::num_sms(); }
+
+int ssb_set_pdl(int on) {
+  const int prev = ssb::pdl_enabled() ? 1 : 0;
+  ssb::g_pdl.store(on ? 1 : 0, std::memory_order_relaxed);
+  return prev;
+}
 
 int ssb_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
                        int64_t height, void* stream) {

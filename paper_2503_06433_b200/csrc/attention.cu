@@ -692,10 +692,7 @@ int launch_decode_p(const CUtensorMap& map, const void* qkv, int ld, int nq, int
   if (ctas_per_sm > 0) per_sm = std::min(per_sm, ctas_per_sm);
   const long items = static_cast<long>(B) * nk;
   const int grid = static_cast<int>(std::min<long>(items, static_cast<long>(std::max(per_sm, 1)) * num_sms()));
-  static const int pdl = [] {
-    const char* e = getenv("SSB_PDL");
-    return e ? atoi(e) : 1;
-  }();
+  const bool pdl = pdl_enabled();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(128);

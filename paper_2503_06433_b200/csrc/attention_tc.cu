@@ -56,17 +56,6 @@ __device__ __forceinline__ uint64_t sdesc_mn_sw128(uint32_t smem_addr, uint32_t 
   return d;
 }
 
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
-      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
-      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
-      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
-      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
-}
-__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
@@ -917,14 +906,18 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
         // S(t) ready; pipe order also means every earlier P.V of this head is done (O stable)
         mbar_wait(&s_full[hh], t & 1);
         tc_fence_after();
+        // raw scores: all four 32-column loads in flight, one wait.  With two
+        // softmax warps per SMSP nothing hides a dependent chain, so the row
+        // max and row sum below run on 8 independent accumulators, and the
+        // softmax scale rides in the exponent's FMA (exp2(s * c - m)).
         float sv[kT];
+        {
+          uint32_t v[kT];
 #pragma unroll
-        for (int c = 0; c < kT / 32; ++c) {
-          uint32_t v[32];
-          tmem_ld32(s_acc + c * 32, v);
+          for (int c = 0; c < kT / 32; ++c) tmem_ld32(s_acc + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + c * 32));
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(v[i]) * scale_log2;
+          for (int i = 0; i < kT; ++i) sv[i] = __uint_as_float(v[i]);
         }
         const int k0 = j * kT;
         if (j == qt || k0 + kT > len) {
@@ -932,9 +925,14 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
           for (int i = 0; i < kT; ++i)
             if (k0 + i > qrow || k0 + i >= len) sv[i] = -INFINITY;
         }
-        float mx = -INFINITY;
+        float m8[8];
 #pragma unroll
-        for (int i = 0; i < kT; ++i) mx = fmaxf(mx, sv[i]);
+        for (int i = 0; i < 8; ++i) m8[i] = sv[i];
+#pragma unroll
+        for (int i = 8; i < kT; ++i) m8[i & 7] = fmaxf(m8[i & 7], sv[i]);
+        const float mraw = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                                 fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+        const float mx = mraw * scale_log2;  // scale_log2 > 0: same argmax
         float corr = 1.f;
         const bool rescale = mx > m_used + kRescaleThreshold;
         if (rescale) {
@@ -952,22 +950,27 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
             tmem_st32(o_acc + c * 32, v);
           }
         }
-        float sum = 0.f;
+        float s8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s8[i] = 0.f;
+        const float nm = -m_used;
         // P over the first 64 columns of this head's S accumulator, 32 keys at a time
 #pragma unroll
         for (int c = 0; c < kT / 32; ++c) {
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float a = fast_exp2(sv[c * 32 + 2 * i] - m_used);
-            const float xb = sv[c * 32 + 2 * i + 1] - m_used;
+            const float a = fast_exp2(fmaf(sv[c * 32 + 2 * i], scale_log2, nm));
+            const float xb = fmaf(sv[c * 32 + 2 * i + 1], scale_log2, nm);
             const float b = (i & kPolyMask) ? exp2_poly(xb) : fast_exp2(xb);
-            sum += a + b;
+            s8[(2 * i) & 7] += a;
+            s8[(2 * i + 1) & 7] += b;
             pk[i] = pack_bf16x2(a, b);
           }
           tmem_st16(s_acc + c * 16, pk);
         }
         tmem_st_wait();
+        const float sum = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
         l = l * corr + sum;
         tc_fence_before();
         __syncwarp();

@@ -101,6 +101,17 @@ struct Params {
   // so a wave starts on the operand slabs the previous wave touched last
   // (still in L2) instead of the ones it evicted first
   int kserp;
+  int num_kb;      // k-blocks of K
+  int unit_tiles;  // output tiles of the schedule (CTA-pair tiles when MC = 2)
+  // stream-K: after sk_dp_rounds rounds of whole tiles (group g: tiles
+  // g + r * groups), the remaining tiles' k-blocks [sk_tile0 * num_kb, ...)
+  // -- sk_W of them -- are cut into `groups` contiguous, equal ranges, one
+  // per group; a tile whose k-blocks span several groups is reduced by the
+  // last contributor to finish (see reduce_parts)
+  int sk;
+  int sk_dp_rounds;
+  int sk_tile0;
+  long long sk_W;
 };
 
 // Grouped rasterisation: kGroupM tiles of the "band" dimension share one
@@ -134,6 +145,78 @@ __device__ __forceinline__ void unit_decode(const Params& p, int u, int& t, int&
     split = v - (v / p.splits) * p.splits;
     nsplit = p.splits;
   }
+}
+
+// One unit of a group's persistent schedule: a unit tile, its k-block range,
+// and -- when the tile is shared (split-K / stream-K) -- the contributors.
+// Contributor j's fp32 partial lives at CTA slot slotA + j * slotS (+ slotD
+// for j = 0) of the workspace, contributors numbered in k order.
+struct Work {
+  int t, kb0, kb1;
+  int nparts, part;
+  int slotA, slotS, slotD;
+};
+
+__device__ __forceinline__ long long sk_start(const Params& p, int g, int G) {
+  return p.sk_W * g / G;
+}
+// the group whose stream-K range holds linear k-block x
+__device__ __forceinline__ int sk_group_of(const Params& p, long long x, int G) {
+  int g = static_cast<int>(x * G / p.sk_W);
+  while (g + 1 < G && sk_start(p, g + 1, G) <= x) ++g;
+  while (g > 0 && sk_start(p, g, G) > x) --g;
+  return g;
+}
+
+__device__ __forceinline__ int num_work(const Params& p, int g, int G) {
+  if (!p.sk) {
+    const int units = p.full_units + (p.unit_tiles - p.full_units) * p.splits;
+    return g < units ? (units - 1 - g) / G + 1 : 0;
+  }
+  const long long s = sk_start(p, g, G), e = sk_start(p, g + 1, G);
+  return p.sk_dp_rounds + (e > s ? static_cast<int>((e - 1) / p.num_kb - s / p.num_kb + 1) : 0);
+}
+
+template <int MC>
+__device__ __forceinline__ void get_work(const Params& p, int g, int G, int i, int crank, Work& w) {
+  if (!p.sk) {
+    int split, nsplit;
+    unit_decode(p, g + i * G, w.t, split, nsplit);
+    w.nparts = nsplit;
+    w.part = split;
+    w.kb0 = nsplit > 1 ? split * p.kb_per_split : 0;
+    w.kb1 = nsplit > 1 ? min(p.num_kb, w.kb0 + p.kb_per_split) : p.num_kb;
+    w.slotA = ((w.t - p.full_units) * MC + crank) * nsplit;
+    w.slotS = 1;
+    w.slotD = 0;
+    return;
+  }
+  if (i < p.sk_dp_rounds) {
+    w.t = g + i * G;
+    w.kb0 = 0;
+    w.kb1 = p.num_kb;
+    w.nparts = 1;
+    w.part = 0;
+    w.slotA = w.slotS = w.slotD = 0;
+    return;
+  }
+  const long long s = sk_start(p, g, G), e = sk_start(p, g + 1, G);
+  const int nkb = p.num_kb;
+  const long long ts = s / nkb + (i - p.sk_dp_rounds);
+  const long long lo = ts * nkb, hi = lo + nkb;
+  w.t = p.sk_tile0 + static_cast<int>(ts);
+  w.kb0 = static_cast<int>((s > lo ? s : lo) - lo);
+  w.kb1 = static_cast<int>((e < hi ? e : hi) - lo);
+  const int ga = sk_group_of(p, lo, G), gb = sk_group_of(p, hi - 1, G);
+  w.nparts = gb - ga + 1;
+  w.part = g - ga;
+  // slots: group g owns two, (2g) for the tile its range starts in and
+  // (2g + 1) for the tile it ends in; contributor 0 may be either, every
+  // later contributor's range starts inside this tile
+  const int w0 = (sk_start(p, ga, G) / nkb == ts) ? 0 : 1;
+  w.slotA = 2 * ga * MC + crank;
+  w.slotS = 2 * MC;
+  w.slotD = w0 * MC;
 }
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
@@ -338,28 +421,122 @@ __device__ __forceinline__ void store_rope(const Params& p, int row, int col_lo,
   }
 }
 
-// Split-K partial layout, per (tile, split): [BN/4 float4 columns][128 rows]
-// of float4, so one warp's store or load of a column group covers 512
-// contiguous bytes (32 rows).  Sum of the `splits` partials of 32 columns
-// (8 float4 groups starting at column group g0) in split order: bitwise
-// independent of which split finished last.
-__device__ __forceinline__ void sum_partials(const float4* base, size_t split_stride4, int splits, int g0,
-                                             float (&f)[32]) {
+// Shared tiles (split-K / stream-K).  Partial layout per CTA slot:
+// [BN/4 float4 columns][128 rows] of float4, so one warp's store or load of a
+// column group covers 512 contiguous bytes (32 rows).  Each epilogue warp
+// (one TMEM lane quadrant = 32 rows) of a contributor:
+//   * if every other contributor already published (counter = nparts - 1),
+//     keeps its accumulator in TMEM and reduces at once;
+//   * else spills its fp32 partial, publishes (fence + counter), and the
+//     warp that brings the counter to nparts reduces -- its own partial
+//     still in TMEM.
+// The reducer adds the partials in contributor (= k) order, its own at its
+// position, and writes the sum back into its TMEM accumulator; the regular
+// whole-tile epilogue then runs from TMEM.  The sum order is fixed by the
+// plan, so the result is bitwise independent of which contributor finished
+// last.  Returns false when another warp will reduce this tile quadrant.
+template <int BN>
+__device__ __forceinline__ bool reduce_parts(const Params& p, const Work& w, int tile, int q, int lane,
+                                             uint32_t tbase) {
+  constexpr size_t stride4 = static_cast<size_t>(kBM) * BN / 4;  // float4 per CTA slot
+  int* ctr = p.counters + tile * 4 + q;
+  float4* ws4 = reinterpret_cast<float4*>(p.ws) + q * 32 + lane;
+  int seen = 0;
+  if (lane == 0) seen = ld_acquire_gpu(ctr);
+  seen = __shfl_sync(0xffffffffu, seen, 0);
+  if (seen != w.nparts - 1) {
+    float4* mine = ws4 + static_cast<size_t>(w.slotA + w.part * w.slotS + (w.part == 0 ? w.slotD : 0)) * stride4;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      uint32_t a[32];
+      tmem_ld32(tbase + c * 32, a);
+      tmem_ld_wait();
 #pragma unroll
-  for (int v = 0; v < 8; ++v) {
-    const float4 x = __ldcg(base + (g0 + v) * kBM);
-    f[4 * v] = x.x; f[4 * v + 1] = x.y; f[4 * v + 2] = x.z; f[4 * v + 3] = x.w;
+      for (int v = 0; v < 8; ++v)
+        __stcg(mine + (c * 8 + v) * kBM, make_float4(__uint_as_float(a[4 * v]), __uint_as_float(a[4 * v + 1]),
+                                                     __uint_as_float(a[4 * v + 2]), __uint_as_float(a[4 * v + 3])));
+    }
+    __threadfence();
+    __syncwarp();
+    int prev = 0;
+    if (lane == 0) prev = atomicAdd(ctr, 1);
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if (prev != w.nparts - 1) return false;
   }
-  for (int s = 1; s < splits; ++s) {
-    const float4* src = base + s * split_stride4;
+  __threadfence();
+  if (lane == 0) *ctr = 0;  // every contributor arrived: zero for the next launch
+  const int n = w.nparts, me = w.part;
+  auto part_ptr = [&](int j) {
+    return ws4 + static_cast<size_t>(w.slotA + j * w.slotS + (j == 0 ? w.slotD : 0)) * stride4;
+  };
+  if (n == 2) {
+    // one other partial: software-pipelined, chunk c+1 in flight while
+    // chunk c is summed and written back
+    const float4* o = part_ptr(1 - me);
     float4 x[8];
 #pragma unroll
-    for (int v = 0; v < 8; ++v) x[v] = __ldcg(src + (g0 + v) * kBM);
+    for (int v = 0; v < 8; ++v) x[v] = __ldcg(o + v * kBM);
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      uint32_t a[32];
+      tmem_ld32(tbase + c * 32, a);
+      float4 y[8];
 #pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      f[4 * v] += x[v].x; f[4 * v + 1] += x[v].y; f[4 * v + 2] += x[v].z; f[4 * v + 3] += x[v].w;
+      for (int v = 0; v < 8; ++v) y[v] = x[v];
+      if (c + 1 < BN / 32) {
+#pragma unroll
+        for (int v = 0; v < 8; ++v) x[v] = __ldcg(o + ((c + 1) * 8 + v) * kBM);
+      }
+      tmem_ld_wait();
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const float yy[4] = {y[v].x, y[v].y, y[v].z, y[v].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float mine_v = __uint_as_float(a[4 * v + k]);
+          a[4 * v + k] = __float_as_uint(me == 0 ? mine_v + yy[k] : yy[k] + mine_v);
+        }
+      }
+      tmem_st32(tbase + c * 32, a);
+    }
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      uint32_t a[32];
+      tmem_ld32(tbase + c * 32, a);
+      tmem_ld_wait();
+      float f[32];
+#pragma unroll 1
+      for (int j = 0; j < n; ++j) {
+        float xs[32];
+        if (j == me) {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) xs[k] = __uint_as_float(a[k]);
+        } else {
+          const float4* src = part_ptr(j);
+          float4 x[8];
+#pragma unroll
+          for (int v = 0; v < 8; ++v) x[v] = __ldcg(src + (c * 8 + v) * kBM);
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            xs[4 * v] = x[v].x; xs[4 * v + 1] = x[v].y; xs[4 * v + 2] = x[v].z; xs[4 * v + 3] = x[v].w;
+          }
+        }
+        if (j == 0) {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) f[k] = xs[k];
+        } else {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) f[k] += xs[k];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 32; ++k) a[k] = __float_as_uint(f[k]);
+      tmem_st32(tbase + c * 32, a);
     }
   }
+  tmem_st_wait();
+  return true;
 }
 
 // MC = CTAs per cluster along M.  With MC = 2 the two CTAs of a cluster
@@ -401,8 +578,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int num_units = p.full_units + (units_m * p.tiles_n - p.full_units) * p.splits;
-  const int num_kb = (p.K + kBK - 1) / kBK;
+  const int nw = num_work(p, cid, nclusters);
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmap_a);
@@ -461,15 +637,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = cid; u < num_units; u += nclusters) {
+      for (int i = 0; i < nw; ++i) {
+        Work w;
+        get_work<MC>(p, cid, nclusters, i, crank, w);
         int um, tn;
-        int t, split, nsplit;
-        unit_decode(p, u, t, split, nsplit);
-        tile_coords(t, units_m, p.tiles_n, p.group_n, p.group_size, um, tn);
+        tile_coords(w.t, units_m, p.tiles_n, p.group_n, p.group_size, um, tn);
         const int tm = um * MC + crank;
-        const int kb0 = nsplit > 1 ? split * p.kb_per_split : 0;
-        const int kb1 = nsplit > 1 ? min(num_kb, kb0 + p.kb_per_split) : num_kb;
-        const bool rev = p.kserp && (((u - cid) / nclusters) & 1);
+        const int kb0 = w.kb0, kb1 = w.kb1;
+        const bool rev = p.kserp && (i & 1);
         for (int i = kb0; i < kb1; ++i) {
           // (the MMA warp only counts k-blocks: the order is the producer's)
           const int kb = rev ? kb1 - 1 - (i - kb0) : i;
@@ -513,14 +688,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = cid; u < num_units; u += nclusters) {
+      for (int i = 0; i < nw; ++i) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        int t, split, nsplit;
-        unit_decode(p, u, t, split, nsplit);
-        const int kb0 = nsplit > 1 ? split * p.kb_per_split : 0;
-        const int kb1 = nsplit > 1 ? min(num_kb, kb0 + p.kb_per_split) : num_kb;
+        Work w;
+        get_work<MC>(p, cid, nclusters, i, crank, w);
+        const int kb0 = w.kb0, kb1 = w.kb1;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -560,10 +734,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = cid; u < num_units; u += nclusters) {
-      int um, tn, t, split, nsplit;
-      unit_decode(p, u, t, split, nsplit);
-      tile_coords(t, units_m, p.tiles_n, p.group_n, p.group_size, um, tn);
+    for (int i = 0; i < nw; ++i) {
+      Work w;
+      get_work<MC>(p, cid, nclusters, i, crank, w);
+      int um, tn;
+      tile_coords(w.t, units_m, p.tiles_n, p.group_n, p.group_size, um, tn);
       const int tm = um * MC + crank;
       const int row = tm * kBM + q * 32 + lane;
       const bool row_ok = row < p.M;
@@ -573,7 +748,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       float ss = 0.f;
-      if (nsplit == 1) {
+      // a shared tile: only the last contributor (holding the sum in TMEM) stores
+      if (w.nparts == 1 || reduce_parts<BN>(p, w, tm * p.tiles_n + tn, q, lane, tbase)) {
         if (p.epi == SSB_EPI_ARGMAX) {
           unsigned long long best = 0;
 #pragma unroll 1
@@ -644,127 +820,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (p.ss_out && row_ok) p.ss_out[static_cast<size_t>(row) * p.tiles_n + tn] = ss;
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (MODE == 2)
-            mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));  // the leader owns the accumulator pipeline
-          else
-            mbar_arrive(&tempty[acc]);
-        }
-      } else {
-        // split-K: spill this split's fp32 partial, release TMEM, and let the
-        // last of the tile quadrant's `splits` warps reduce + run the epilogue
-        const int tile = tm * p.tiles_n + tn;
-        // partial slots are compact over the split unit tiles (x2 CTAs of a pair)
-        const size_t slot0 = static_cast<size_t>((t - p.full_units) * MC + crank) * nsplit;
-        const size_t split_stride4 = static_cast<size_t>(kBM) * BN / 4;  // float4 per (tile, split)
-        float4* wbase = reinterpret_cast<float4*>(p.ws) + (slot0 + split) * split_stride4 + q * 32 + lane;
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t a[32];
-          tmem_ld32(tbase + c * 32, a);
-          tmem_ld_wait();
-#pragma unroll
-          for (int v = 0; v < 8; ++v)
-            __stcg(wbase + (c * 8 + v) * kBM,
-                   make_float4(__uint_as_float(a[4 * v]), __uint_as_float(a[4 * v + 1]),
-                               __uint_as_float(a[4 * v + 2]), __uint_as_float(a[4 * v + 3])));
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (MODE == 2)
-            mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
-          else
-            mbar_arrive(&tempty[acc]);
-        }
-        __threadfence();
-        __syncwarp();
-        int prev = 0;
-        if (lane == 0) prev = atomicAdd(&p.counters[tile * 4 + q], 1);
-        prev = __shfl_sync(0xffffffffu, prev, 0);
-        if (prev == nsplit - 1) {
-          __threadfence();
-          if (lane == 0) p.counters[tile * 4 + q] = 0;  // every split arrived: reset for the next launch
-          const float4* rbase = reinterpret_cast<const float4*>(p.ws) + slot0 * split_stride4 + q * 32 + lane;
-          if (p.epi == SSB_EPI_ARGMAX) {
-            unsigned long long best = 0;
-#pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-              float f[32];
-              sum_partials(rbase, split_stride4, nsplit, c * 8, f);
-              if (p.ss_in) scale32(f, rs);
-              argmax_cols(p, tn * BN + c * 32, f, best);
-            }
-            if (row_ok && best) atomicMax(reinterpret_cast<unsigned long long*>(p.C) + row, best);
-          } else if (p.epi == SSB_EPI_ROPE_KV) {
-#pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-              if (c & 2) continue;
-              float fl[32], fh[32];
-              sum_partials(rbase, split_stride4, nsplit, c * 8, fl);
-              sum_partials(rbase, split_stride4, nsplit, (c + 2) * 8, fh);
-              if (p.ss_in) {
-                scale32(fl, rs);
-                scale32(fh, rs);
-              }
-              if (row_ok && tn * BN + c * 32 < p.N) store_rope(p, row, tn * BN + c * 32, fl, fh);
-            }
-          } else if (p.epi == SSB_EPI_SILU_MUL) {
-#pragma unroll 1
-            for (int c = 0; c < BN / 64; ++c) {
-              float g[32], v[32];
-              sum_partials(rbase, split_stride4, nsplit, c * 16, g);
-              sum_partials(rbase, split_stride4, nsplit, c * 16 + 8, v);
-              if (p.ss_in) {
-                scale32(g, rs);
-                scale32(v, rs);
-              }
-              if (row_ok) store_silu(p, row, (tn * BN) / 2 + c * 32, g, v);
-            }
-          } else if (nsplit == 2) {
-            // software-pipelined: the next chunk's two partials are in flight
-            // while this chunk is converted and stored (otherwise every chunk
-            // costs a full L2 round trip after the previous chunk's stores)
-            float4 x0[8], x1[8];
-#pragma unroll
-            for (int v = 0; v < 8; ++v) {
-              x0[v] = __ldcg(rbase + v * kBM);
-              x1[v] = __ldcg(rbase + split_stride4 + v * kBM);
-            }
-#pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-              float f[32];
-#pragma unroll
-              for (int v = 0; v < 8; ++v) {
-                f[4 * v] = x0[v].x + x1[v].x;
-                f[4 * v + 1] = x0[v].y + x1[v].y;
-                f[4 * v + 2] = x0[v].z + x1[v].z;
-                f[4 * v + 3] = x0[v].w + x1[v].w;
-              }
-              if (c + 1 < BN / 32) {
-#pragma unroll
-                for (int v = 0; v < 8; ++v) {
-                  x0[v] = __ldcg(rbase + ((c + 1) * 8 + v) * kBM);
-                  x1[v] = __ldcg(rbase + split_stride4 + ((c + 1) * 8 + v) * kBM);
-                }
-              }
-              if (p.ss_in) scale32(f, rs);
-              if (row_ok) store_cols(p, row, tn * BN + c * 32, f, ss);
-            }
-            if (p.ss_out && row_ok) p.ss_out[static_cast<size_t>(row) * p.tiles_n + tn] = ss;
-          } else {
-#pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-              float f[32];
-              sum_partials(rbase, split_stride4, nsplit, c * 8, f);
-              if (p.ss_in) scale32(f, rs);
-              if (row_ok) store_cols(p, row, tn * BN + c * 32, f, ss);
-            }
-            if (p.ss_out && row_ok) p.ss_out[static_cast<size_t>(row) * p.tiles_n + tn] = ss;
-          }
-        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (MODE == 2)
+          mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));  // the leader owns the accumulator pipeline
+        else
+          mbar_arrive(&tempty[acc]);
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
@@ -794,10 +857,29 @@ int gemm_policy_mode() {
   return mode;
 }
 
+// Stream-K layout of a persistent schedule of `unit_tiles` tiles over
+// `groups` CTA groups: whole-tile rounds while at least two rounds remain,
+// then the last 1-2 rounds' k-blocks split evenly over the groups.  Off when
+// the tiles already fill whole rounds or the range would be too fine.
+struct SKLayout {
+  int dp_rounds, tile0;
+  long long W;
+  bool on;
+};
+SKLayout sk_layout(long unit_tiles, int num_kb, long groups) {
+  SKLayout l{0, 0, 0, false};
+  if (unit_tiles >= groups && unit_tiles % groups == 0) return l;
+  l.dp_rounds = unit_tiles > groups ? static_cast<int>(unit_tiles / groups) - 1 : 0;
+  l.tile0 = static_cast<int>(l.dp_rounds * groups);
+  l.W = static_cast<long long>(unit_tiles - l.tile0) * num_kb;
+  l.on = l.W >= 4LL * groups;
+  return l;
+}
+
 template <int BN, int MODE>
 int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, int K, int lda,
            int ldb, int ldc, int ldr, int epi, cudaStream_t stream, int max_ctas, int splits, void* ws,
-           const RopeKV* rk, int arg_base, bool tail, ssb_rownorm* rn) {
+           const RopeKV* rk, int arg_base, bool tail, ssb_rownorm* rn, bool sk) {
   using C = Cfg<BN, MODE>;
   constexpr int MC = MODE ? 2 : 1;
   CUtensorMap ta, tb;
@@ -865,10 +947,27 @@ int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, 
     p.full_units = static_cast<int>(unit_tiles);
   else
     p.full_units = tail ? static_cast<int>((unit_tiles / groups) * groups) : 0;
+  p.num_kb = num_kb;
+  p.unit_tiles = static_cast<int>(unit_tiles);
+  p.sk = 0;
+  p.sk_dp_rounds = p.sk_tile0 = 0;
+  p.sk_W = 0;
+  if (sk) {
+    const SKLayout l = sk_layout(unit_tiles, num_kb, groups);
+    if (l.on) {
+      p.sk = 1;
+      p.sk_dp_rounds = l.dp_rounds;
+      p.sk_tile0 = l.tile0;
+      p.sk_W = l.W;
+      p.splits = 1;
+      p.full_units = static_cast<int>(unit_tiles);
+      p.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kCounterBytes);
+    }
+  }
   const long units = p.full_units + (unit_tiles - p.full_units) * p.splits;
-  grid = static_cast<int>(std::min<long>(groups, units)) * MC;
+  grid = p.sk ? static_cast<int>(groups) * MC : static_cast<int>(std::min<long>(groups, units)) * MC;
   {
-    static const int pdl = gemm_env("SSB_PDL", 1);
+    const bool pdl = pdl_enabled();
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
@@ -898,6 +997,7 @@ int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, 
 struct Plan {
   int mode, bn, splits;
   int tail;  // split only the tiles of the last partial wave
+  int sk;    // stream-K (splits = 1)
 };
 
 // Tiles (128-row, including a pair's phantom tile when tiles_m is odd).
@@ -909,9 +1009,15 @@ size_t plan_tiles(int M, int N, const Plan& pl) {
 // Workspace bytes of a split plan; SIZE_MAX when the tile counters do not fit
 // the fixed counter area.
 size_t plan_ws_bytes(int M, int N, const Plan& pl, int sms) {
-  if (pl.splits <= 1) return 0;
   const int MC = pl.mode ? 2 : 1;
   const size_t tiles = plan_tiles(M, N, pl);
+  if (pl.sk) {
+    // two partial slots per CTA of every group
+    if (tiles * 4 * sizeof(int) > kCounterBytes) return SIZE_MAX;
+    const size_t groups = std::max(sms / MC, 1);
+    return kCounterBytes + 2 * groups * MC * kBM * pl.bn * sizeof(float);
+  }
+  if (pl.splits <= 1) return 0;
   if (tiles * 4 * sizeof(int) > kCounterBytes) return SIZE_MAX;
   size_t split_tiles = tiles;
   if (pl.tail) {
@@ -931,10 +1037,27 @@ size_t plan_ws_bytes(int M, int N, const Plan& pl, int sms) {
 // tools/bench_kernels.py --what splitk (Llama decode shapes at M = 256/512,
 // TP1 and TP8, and prefill shapes); the fitted plan is within 1.2x of the
 // best forced configuration on every swept shape (profiles/ summary).
+double plan_kb_us(const Plan& pl) {
+  if (pl.mode == 2)
+    return pl.bn >= 256 ? 0.3839 : pl.bn >= 224 ? 0.3282 : pl.bn >= 192 ? 0.425 : pl.bn >= 128 ? 0.2417 : 1.0;
+  return pl.bn >= 256 ? 2.4031 : pl.bn >= 224 ? 1.435 : pl.bn >= 192 ? 0.3997 : pl.bn >= 128 ? 0.2308 : 1.0;
+}
+
 double plan_cost(int M, int N, int K, int sms, const Plan& pl) {
   const int MC = pl.mode ? 2 : 1;
   const int tm = (M + kBM - 1) / kBM;
   const int kb = (K + kBK - 1) / kBK;
+  if (pl.sk) {
+    const long unit_tiles = static_cast<long>((tm + MC - 1) / MC) * ((N + pl.bn - 1) / pl.bn);
+    const long groups = std::max(1, sms / MC);
+    const SKLayout l = sk_layout(unit_tiles, kb, groups);
+    if (!l.on) return 1e30;
+    // whole-tile rounds, then an even share of the stream-K k-blocks, plus
+    // one partial spill + reduction (~ a split-K fix-up) on the tail
+    const double per = static_cast<double>(l.W) / groups;
+    const double bytes = 2.0 * groups * MC * kBM * pl.bn * 4.0;
+    return 10.86 + (l.dp_rounds * kb + per) * plan_kb_us(pl) + 4.0 + 0.03 * bytes / 1e6;
+  }
   const int kbs = (kb + pl.splits - 1) / pl.splits;
   const int splits = (kb + kbs - 1) / kbs;
   if (pl.tail) {
@@ -1026,8 +1149,25 @@ Plan choose_plan(int M, int N, int K, int epi, int sms, size_t ws_bytes) {
       for (int tail = 0; tail <= 0; ++tail) {
         for (int sp = tail ? 2 : 1; sp <= 16; ++sp) {
           if (sp > 1 && (kb / sp < 4 || no_split)) break;
-          Plan pl{mode, bn, sp, tail};
+          Plan pl{mode, bn, sp, tail, 0};
           if (sp > 1 && plan_ws_bytes(M, N, pl, sms) > ws_bytes) break;
+          const double t = plan_cost(M, N, K, sms, pl);
+          if (t < best_t * 0.995) {
+            best_t = t;
+            best = pl;
+          }
+        }
+      }
+      // stream-K is never chosen automatically: measured on every Llama
+      // decode shape at M = 512 (profiles/r02/gemm_plan_sweep_streamk.jsonl)
+      // it is 6-14 us SLOWER than the best whole-tile / split-K plan even
+      // where it fills all 148 SMs instead of 64-128 (o_proj: 35-43 us vs
+      // 28.7).  Kept behind SSB_GEMM_STREAMK for the record (SSB_GEMM_AUTO_SK=1
+      // re-enables it in the model search).
+      static const int auto_sk = gemm_env("SSB_GEMM_AUTO_SK", 0);
+      if (auto_sk && M <= 2048 && !no_split) {
+        Plan pl{mode, bn, 1, 0, 1};
+        if (plan_ws_bytes(M, N, pl, sms) <= ws_bytes) {
           const double t = plan_cost(M, N, K, sms, pl);
           if (t < best_t * 0.995) {
             best_t = t;
@@ -1069,18 +1209,23 @@ int gemm_entry(const void* A, const void* B, void* C, const void* R, int M, int 
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int sms = max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms();
-  Plan pl{0, block_n & 0xFFFF, 1, 0};
+  Plan pl{0, block_n & 0xFFFF, 1, 0, 0};
   const int forced_split = (block_n >> SSB_GEMM_SPLIT_SHIFT) & 0xFF;
   const int forced_tail = (block_n & SSB_GEMM_TAIL) ? 1 : 0;
-  if (pl.bn == 0 && !(block_n & (SSB_GEMM_MC1 | SSB_GEMM_MC2 | SSB_GEMM_2SM)) && forced_split == 0) {
+  const int forced_sk = (block_n & SSB_GEMM_STREAMK) ? 1 : 0;
+  if (pl.bn == 0 && !(block_n & (SSB_GEMM_MC1 | SSB_GEMM_MC2 | SSB_GEMM_2SM)) && forced_split == 0 && !forced_sk) {
     pl = choose_plan(M, N, K, epilogue, sms, static_cast<size_t>(ws_bytes));
   } else {
     pl.mode = (block_n & SSB_GEMM_2SM) ? 2 : (block_n & SSB_GEMM_MC2) ? 1 : 0;
     if (pl.bn == 0) pl.bn = 256;
-    pl.splits = forced_split ? forced_split : 1;
-    pl.tail = forced_tail;
+    pl.splits = forced_split && !forced_sk ? forced_split : 1;
+    pl.tail = forced_tail && !forced_sk;
+    pl.sk = forced_sk;
     if (pl.mode == 2 && M <= kBM) pl.mode = 0;
   }
+  if (pl.sk && plan_ws_bytes(M, N, pl, sms) > static_cast<size_t>(ws_bytes))
+    return fail_arg("ssb_gemm_bf16: stream-K needs %zu workspace bytes, have %lld", plan_ws_bytes(M, N, pl, sms),
+                    static_cast<long long>(ws_bytes));
   if (epilogue == SSB_EPI_SILU_MUL && pl.bn % 64)
     return fail_arg("ssb_gemm_bf16: SiLU epilogue needs block_n %% 64 == 0");
   if (epilogue == SSB_EPI_ROPE_KV && pl.bn % 128)
@@ -1100,11 +1245,11 @@ int gemm_entry(const void* A, const void* B, void* C, const void* R, int M, int 
 #define SSB_GEMM_CASE(BN_)                                                                              \
   case BN_:                                                                                            \
     return pl.mode == 2   ? launch<BN_, 2>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas, \
-                                           pl.splits, workspace, rk, arg_base, pl.tail != 0, rn)           \
+                                           pl.splits, workspace, rk, arg_base, pl.tail != 0, rn, pl.sk != 0)           \
            : pl.mode == 1 ? launch<BN_, 1>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas, \
-                                           pl.splits, workspace, rk, arg_base, pl.tail != 0, rn)           \
+                                           pl.splits, workspace, rk, arg_base, pl.tail != 0, rn, pl.sk != 0)           \
                           : launch<BN_, 0>(A, B, C, R, M, N, K, lda, ldb, ldc, ldr, epilogue, s, max_ctas, \
-                                           pl.splits, workspace, rk, arg_base, pl.tail != 0, rn);
+                                           pl.splits, workspace, rk, arg_base, pl.tail != 0, rn, pl.sk != 0);
   switch (pl.bn) {
     SSB_GEMM_CASE(256)
     SSB_GEMM_CASE(224)
@@ -1145,7 +1290,7 @@ extern "C" int64_t ssb_gemm_plan(int M, int N, int K, int epilogue, int max_ctas
   if (out_plan) {
     out_plan[0] = pl.mode;
     out_plan[1] = pl.bn;
-    out_plan[2] = pl.tail ? -pl.splits : pl.splits;  // negative: tail split
+    out_plan[2] = pl.sk ? 0 : pl.tail ? -pl.splits : pl.splits;  // negative: tail split; 0: stream-K
   }
   return static_cast<int64_t>(plan_ws_bytes(M, N, pl, sms));
 }

@@ -240,13 +240,13 @@ int ssb_rmsnorm(const void* x, int ldx, const int32_t* row_idx, const void* w, v
   }
   // optional programmatic dependent launch: the CTAs become resident while
   // the producing GEMM drains and start the moment it completes
-  static const int pdl = [] {
-    const char* e = getenv("SSB_PDL");
-    const char* n = getenv("SSB_PDL_NORM");
+  static const int pdl_norm = [] {
     // measured +0.15 % batch time with it on (its 512 waiting CTAs delay the
     // next GEMM's residency), so off unless SSB_PDL_NORM=1
-    return (e ? atoi(e) : 1) && (n ? atoi(n) : 0);
+    const char* n = getenv("SSB_PDL_NORM");
+    return n ? atoi(n) : 0;
   }();
+  const bool pdl = pdl_enabled() && pdl_norm;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(rows);
   cfg.blockDim = dim3(kNormThreads);

@@ -48,6 +48,7 @@ struct ARPeers {
   const __nv_bfloat16* part[kARMaxRanks];
   __nv_bfloat16* x[kARMaxRanks];
   __nv_bfloat16* h[kARMaxRanks];
+  float* ss[kARMaxRanks];  // folded-norm variant: per-row sum of squares of x (no h)
   uint32_t* sig[kARMaxRanks];
 };
 
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(kARThreads)
         }
       }
     }
-    if (gamma == nullptr) continue;
+    if (gamma == nullptr && P.ss[0] == nullptr) continue;
     ss = warp_sum(ss);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
     __syncthreads();
@@ -176,6 +177,13 @@ __global__ void __launch_bounds__(kARThreads)
       if (threadIdx.x == 0) red[0] = t;
     }
     __syncthreads();
+    if (P.ss[0] != nullptr) {
+      // folded norm: the consumer GEMMs scale their rows by 1/rms from this
+      // sum (ssb_rownorm, one part), the gains live in their weights
+      if (threadIdx.x < N) __stcg(P.ss[threadIdx.x] + row, red[0]);
+      __syncthreads();  // red[] is rewritten by the next row
+      continue;
+    }
     const float inv = 1.0f / sqrtf(__fadd_rn(__fdiv_rn(red[0], static_cast<float>(hidden)), eps));
     __syncthreads();  // red[] is rewritten by the next row
     const uint4* gr = reinterpret_cast<const uint4*>(gamma);
@@ -243,10 +251,11 @@ size_t ssb_tp_signal_bytes(void) {
   return (ssb::kARSlots + ssb::kARMaxBlocks) * sizeof(uint32_t);
 }
 
-int ssb_tp_allreduce_rmsnorm(const uint64_t* part_addrs, const uint64_t* x_addrs, const uint64_t* h_addrs,
-                             const uint64_t* sig_addrs, int nranks, int rank, int rows, int hidden, int ld,
-                             const void* gamma, float eps, uint32_t epoch, int max_blocks, uint32_t* err,
-                             void* stream) {
+namespace {
+int tp_combine_launch(const uint64_t* part_addrs, const uint64_t* x_addrs, const uint64_t* h_addrs,
+                      const uint64_t* ss_addrs, const uint64_t* sig_addrs, int nranks, int rank, int rows,
+                      int hidden, int ld, const void* gamma, float eps, uint32_t epoch, int max_blocks,
+                      uint32_t* err, void* stream) {
   using namespace ssb;
   SSB_REQUIRE(nranks >= 1 && nranks <= kARMaxRanks, "ssb_tp_allreduce_rmsnorm: nranks %d not in [1, %d]", nranks,
               kARMaxRanks);
@@ -264,8 +273,10 @@ int ssb_tp_allreduce_rmsnorm(const uint64_t* part_addrs, const uint64_t* x_addrs
     P.part[p] = reinterpret_cast<const __nv_bfloat16*>(part_addrs[p]);
     P.x[p] = reinterpret_cast<__nv_bfloat16*>(x_addrs[p]);
     P.h[p] = gamma ? reinterpret_cast<__nv_bfloat16*>(h_addrs[p]) : nullptr;
+    P.ss[p] = ss_addrs ? reinterpret_cast<float*>(ss_addrs[p]) : nullptr;
     P.sig[p] = reinterpret_cast<uint32_t*>(sig_addrs[p]);
-    SSB_REQUIRE(aligned16(P.part[p]) && aligned16(P.x[p]) && (!gamma || aligned16(P.h[p])) && P.sig[p],
+    SSB_REQUIRE(aligned16(P.part[p]) && aligned16(P.x[p]) && (!gamma || aligned16(P.h[p])) && P.sig[p] &&
+                    (!ss_addrs || P.ss[p]),
                 "ssb_tp_allreduce_rmsnorm: rank %d buffers must be 16-byte aligned", p);
   }
   // the grid depends only on (rows, nranks, max_blocks): every rank launches
@@ -290,6 +301,23 @@ int ssb_tp_allreduce_rmsnorm(const uint64_t* part_addrs, const uint64_t* x_addrs
 #undef SSB_AR_CASE
   }
   return check_launch("ssb_tp_allreduce_rmsnorm");
+}
+}  // namespace
+
+int ssb_tp_allreduce_rmsnorm(const uint64_t* part_addrs, const uint64_t* x_addrs, const uint64_t* h_addrs,
+                             const uint64_t* sig_addrs, int nranks, int rank, int rows, int hidden, int ld,
+                             const void* gamma, float eps, uint32_t epoch, int max_blocks, uint32_t* err,
+                             void* stream) {
+  return tp_combine_launch(part_addrs, x_addrs, h_addrs, nullptr, sig_addrs, nranks, rank, rows, hidden, ld, gamma,
+                           eps, epoch, max_blocks, err, stream);
+}
+
+int ssb_tp_allreduce_rowss(const uint64_t* part_addrs, const uint64_t* x_addrs, const uint64_t* ss_addrs,
+                           const uint64_t* sig_addrs, int nranks, int rank, int rows, int hidden, int ld,
+                           uint32_t epoch, int max_blocks, uint32_t* err, void* stream) {
+  SSB_REQUIRE(ss_addrs, "ssb_tp_allreduce_rowss: null ss address table");
+  return tp_combine_launch(part_addrs, x_addrs, nullptr, ss_addrs, sig_addrs, nranks, rank, rows, hidden, ld, nullptr,
+                           0.f, epoch, max_blocks, err, stream);
 }
 
 int ssb_tp_argmax_keys(const uint64_t* key_addrs, const uint64_t* sig_addrs, int nranks, int rank, int rows,

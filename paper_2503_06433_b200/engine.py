@@ -864,6 +864,12 @@ class _Engine:
         replica sums (the last stage's tensor rank 0 contributes, every other
         rank zeros; the prefill first tokens are replica-wide already and
         enter through the same rank)."""
+        if self.comm.size > 1:
+            # every rank has issued all of its kernels before this one blocks
+            # on a device->host copy: virtual ranks share the process, and a
+            # pageable D2H copy can hold the driver while a peer still has to
+            # launch the other half of a fused combine's barrier
+            self.comm.barrier()
         if not self.rows:
             return
         flat = torch.cat([t for _, t in self.rows])

@@ -394,3 +394,22 @@ def tp_allreduce_rmsnorm(part_addrs, x_addrs, h_addrs, sig_addrs, rank: int, row
          _lib.uint64_array(h_addrs) if h_addrs is not None else None, _lib.uint64_array(sig_addrs), n, rank, rows,
          hidden, hidden, gamma.data_ptr() if gamma is not None else None, eps, epoch, max_blocks,
          err.data_ptr() if err is not None else None, _stream())
+
+
+def tp_allreduce_rowss(part_addrs, x_addrs, ss_addrs, sig_addrs, rank: int, rows: int, hidden: int, epoch: int,
+                       max_blocks: int, err: torch.Tensor | None = None) -> None:
+    """x = sum over ranks of part into every rank's x, and the per-row fp32
+    sum of squares of x into every rank's ss (the folded-norm combine,
+    C-ABI ssb_tp_allreduce_rowss).  Address lists as for
+    :func:`tp_allreduce_rmsnorm` (plain lists or prebuilt ctypes arrays)."""
+    def arr(a):
+        return a if isinstance(a, ctypes.Array) else _lib.uint64_array(a)
+
+    call("ssb_tp_allreduce_rowss", arr(part_addrs), arr(x_addrs), arr(ss_addrs), arr(sig_addrs), len(part_addrs),
+         rank, rows, hidden, hidden, epoch, max_blocks, err.data_ptr() if err is not None else None, _stream())
+
+
+def set_pdl(on: bool) -> bool:
+    """Programmatic dependent launch on/off for the library's launches
+    (C-ABI ssb_set_pdl); returns the previous setting."""
+    return bool(load().ssb_set_pdl(1 if on else 0))

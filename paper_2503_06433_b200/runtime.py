@@ -69,6 +69,39 @@ def _copy_desc_rows(entries: list[tuple[int, int, int, int, int, int]]) -> tuple
     return out, cum
 
 
+def runtime_reserve(arch: LlamaArch, gpu: int, cfg_p: ParallelismConfig, cfg_d: ParallelismConfig,
+                    max_prefill_tokens: int, block_size: int = 64, ws_bytes: int = 64 << 20,
+                    chunk_bytes: int = 256 << 20) -> dict:
+    """Bytes one GPU needs beyond its weights and its KV pool at the peak of
+    a run, by component:
+      * weight_transient: a weight re-partition holds the new arena next to
+        the old one, plus two chunk buffers each way (SSB_RESHARD_CHUNK_MB);
+        the KV re-shard stages 256 blocks of its rectangles twice each way
+        (the larger of the two; they do not overlap);
+      * activations: a max_prefill_tokens forward (h, x, qkv, attention out,
+        gate/up product, row sums) and the fp32 logits of its last rows
+        (decode buffers are smaller);
+      * workspaces: two GEMM split-K / stream-K workspaces, the fused-TP peer
+        arena and host-tier staging;
+      * slack: 2 GiB for the allocator."""
+    a = arch
+    mx = 0
+    cfgs = {cfg_p, cfg_d}
+    if len(cfgs) > 1:
+        new = max(weight_layout(a, c.tp, c.pp, gpu).arena_elems for c in cfgs) * 2
+        mx = new + 4 * chunk_bytes
+        blk = max(kv_geometry(a, c.tp, c.pp, 1, block_size).block_elems for c in cfgs) * 2
+        mx = max(mx, 4 * 256 * blk)
+    T = max_prefill_tokens
+    tp = min(c.tp for c in cfgs)
+    act = T * (2 * a.hidden + a.qkv_dim // tp + a.num_query_heads * a.head_dim // tp + a.ffn // tp) * 2
+    act += 2 * T * (-(-a.hidden // 64)) * 4 + 2 * T * 4 * (a.vocab // tp) // max(T // 512, 1)
+    ws = 2 * ws_bytes + 3 * T * a.hidden * 2
+    slack = 2 << 30
+    return {"weight_transient": int(mx), "activations": int(act), "workspaces": int(ws), "slack": slack,
+            "total": int(mx + act + ws + slack)}
+
+
 @dataclass
 class LayoutState:
     cfg: ParallelismConfig
@@ -147,6 +180,9 @@ class Worker:
         # GEMMs emit row sums of squares, the consumers scale rows by 1/rms,
         # the gains live in the consumer weights (fold_gains)
         self.fold_norm = os.environ.get("SSB_FOLD_NORM", "1") != "0"
+        # TP decode with the folded norm: the combine broadcasts x plus one
+        # fp32 row sum of squares instead of x and h (half the NVLink stores)
+        self.tp_fold = os.environ.get("SSB_TP_FOLD", "1") != "0"
         # decode steps replayed from CUDA graphs (per batch size)
         self.cuda_graphs = os.environ.get("SSB_CUDA_GRAPH", "1") != "0"
         self._graphs: dict = {}
@@ -555,6 +591,11 @@ class Worker:
         from . import tpcombine
         from .comm import ThreadComm
 
+        if isinstance(tp, ThreadComm):
+            # virtual ranks share the GPU: a rank's GEMM launched early by
+            # programmatic dependent launch would hold SMs (waiting on its own
+            # combine) that a peer's producer needs to reach the same barrier
+            ops.set_pdl(False)
         blocks = self.fused_tp_blocks or (
             16 if isinstance(tp, ThreadComm) else torch.cuda.get_device_properties(self.device).multi_processor_count)
         return tpcombine.get_arena(self._tp_arenas, tp, self.device, self.arch.hidden, rows, blocks)
@@ -567,7 +608,7 @@ class Worker:
         return self.w("final_norm") if final else None
 
     def _block(self, x: torch.Tensor, layer: int, attn_fn, buf: dict, rope: tuple, cap: int = 0, ar=None,
-               h_ready: bool = False, final: bool = False) -> bool:
+               h_ready: bool = False, final: bool = False, fold: bool = False) -> bool:
         """One transformer layer on x (in place); attn_fn(qkv, layer_local) -> attn out.
         ``rope`` = (positions, slots) of the rows: RoPE and the paged K/V
         append run in the QKV GEMM's epilogue (head_dim 128) or as a separate
@@ -578,8 +619,12 @@ class Worker:
         produces the NEXT rmsnorm (ar.h): ``h_ready`` says this layer's input
         norm is already in ar.h; returns whether the next one is (the
         combine after the MLP applies the next layer's attn_norm, or
-        final_norm on the last layer when ``final``)."""
+        final_norm on the last layer when ``final``).  ``fold`` (decode
+        under a pure TP layout): the combines produce x and its row sums of
+        squares (ar.ss) instead of h, and the consumer GEMMs apply 1/rms."""
         if ar is not None:
+            if fold:
+                return self._block_fused_folded(x, layer, attn_fn, buf, rope, cap, ar, h_ready)
             return self._block_fused(x, layer, attn_fn, buf, rope, cap, ar, h_ready, final)
         st = self.state
         if self.fold_norm and st.tp_comm.size == 1:
@@ -686,6 +731,49 @@ class Worker:
         g = self._next_gamma(layer, final)
         ar.combine(T, g, eps)
         return g is not None
+
+    def _block_fused_folded(self, x, layer, attn_fn, buf, rope, cap, ar, ss_ready: bool) -> bool:
+        """TP layer with the fused combine AND the folded norm: each combine
+        leaves x and its per-row sum of squares (ar.ss) on every rank; the
+        QKV and gate/up GEMMs read x and scale their rows by 1/rms (gains
+        folded into their weights, fold_gains).  ``ss_ready``: ar.ss holds
+        this layer's input sums (else its attn_norm runs as a kernel)."""
+        st = self.state
+        eps = self.arch.rms_eps
+        hid = self.arch.hidden
+        p = f"L{layer}."
+        lead = st.rank == 0
+        ws = buf["ws"]
+        local = layer - st.weights.layer_begin
+        nq, nk = st.weights.n_q_heads, st.weights.n_kv_heads
+        pos, slots = rope
+        geo = self.geometry().as_tuple()
+        T = x.shape[0]
+        part, ss = ar.part[:T], ar.ss[:T].view(T, 1)
+        if ss_ready:
+            a_in, rn = x, ops.row_norm(ss_in=ss, ss_in_parts=1, hidden=hid, eps=eps)
+        else:
+            a_in, rn = ops.rmsnorm(x, self.w(p + "attn_norm"), eps, out=ar.h[:T]), None
+        if self.fuse_rope and self.arch.head_dim == 128:
+            qkv = ops.gemm_qkv_rope_kv(a_in, self.w(p + "wqkv"), buf["qkv"], nq, nk, pos, self.rope_cos,
+                                       self.rope_sin, self.pool, geo, local, slots, max_ctas=cap, workspace=ws,
+                                       rownorm=rn)
+        else:
+            qkv = ops.gemm(a_in, self.w(p + "wqkv"), out=buf["qkv"], max_ctas=cap, workspace=ws, rownorm=rn)
+            ops.rope_kv_append(qkv, nq, nk, pos, self.rope_cos, self.rope_sin, self.pool, geo, local, slots)
+        attn = attn_fn(qkv, local)
+        ops.gemm(attn, self.w(p + "wo"), out=part, residual=x if lead else None, max_ctas=cap, workspace=ws)
+        ar.combine_ss(T)
+        rn_m = ops.row_norm(ss_in=ss, ss_in_parts=1, hidden=hid, eps=eps)
+        act = ops.gemm(x, self.w(p + "w13"), out=buf["act"], silu_mul=True, max_ctas=cap, workspace=ws,
+                       rownorm=rn_m)
+        ops.gemm(act, self.w(p + "w2"), out=part, residual=x if lead else None, max_ctas=cap, workspace=ws)
+        ar.combine_ss(T)
+        return True
+
+    def _tp_fold(self, ar) -> bool:
+        """Decode under a pure TP layout with the fused combine runs folded."""
+        return ar is not None and self.fold_norm and self.tp_fold and self.state.cfg.pp == 1
 
     def _reduce_into(self, x: torch.Tensor) -> None:
         """Row-parallel combine: rank 0 added the residual in its GEMM epilogue,
@@ -882,10 +970,14 @@ class Worker:
                 x = buf.get("x")
                 if x is None or x.shape[0] != n:
                     x = buf["x"] = torch.empty(n, a.hidden, dtype=torch.bfloat16, device=self.device)
+            fold = self._tp_fold(ar)
             if first:
                 if ar is not None:
                     ops.embedding(v["tok"], self.w("embed"), st.weights.vocab_begin, ar.part[:n])
-                    ar.combine(n, self.w(f"L{st.weights.layer_begin}.attn_norm"), a.rms_eps)
+                    if fold:
+                        ar.combine_ss(n)
+                    else:
+                        ar.combine(n, self.w(f"L{st.weights.layer_begin}.attn_norm"), a.rms_eps)
                     h_ready = True
                 else:
                     ops.embedding(v["tok"], self.w("embed"), st.weights.vocab_begin, x)
@@ -900,12 +992,14 @@ class Worker:
 
             for layer in self._layers():
                 h_ready = self._block(x, layer, attn, buf, (v["pos"], v["slot"]), ar=ar, h_ready=h_ready,
-                                      final=last)
+                                      final=last, fold=fold)
             if not last:
                 self.replica_comm.send(x, st.pp_next)
                 continue
             rn = None
-            if ar is not None and h_ready:
+            if ar is not None and h_ready and fold:
+                h, rn = x, ops.row_norm(ss_in=ar.ss[:n].view(n, 1), ss_in_parts=1, hidden=a.hidden, eps=a.rms_eps)
+            elif ar is not None and h_ready:
                 h = ar.h[:n]
             elif self.fold_norm and st.tp_comm.size == 1 and h_ready:
                 h, rn = x, self._final_rownorm(buf, n, int(h_ready))
@@ -922,29 +1016,9 @@ class Worker:
 
     def runtime_reserve_bytes(self, cfg_p: ParallelismConfig, cfg_d: ParallelismConfig, max_prefill_tokens: int) -> int:
         """HBM this GPU needs beyond its weights and KV pool at the peak of a
-        run (ADVICE: the pool must leave room for it):
-          * a weight re-partition holds the new arena next to the old one,
-            plus two chunk buffers each way (SSB_RESHARD_CHUNK_MB);
-          * the KV re-shard stages 256 blocks of its rectangles twice each way;
-          * prefill activations of a max_prefill_tokens forward (h, x, qkv,
-            attention out, gate/up product, row sums) and the fp32 logits of
-            its last rows; decode buffers are smaller;
-          * GEMM split-K workspaces, the fused-TP peer arena, host-tier
-            staging, and 2 GiB of allocator slack."""
-        a = self.arch
-        mx = 0
-        cfgs = {cfg_p, cfg_d}
-        if len(cfgs) > 1:
-            new = max(weight_layout(a, c.tp, c.pp, self.gpu).arena_elems for c in cfgs) * 2
-            mx = new + 4 * self.RESHARD_CHUNK_BYTES
-            blk = max(kv_geometry(a, c.tp, c.pp, 1, self.block_size).block_elems for c in cfgs) * 2
-            mx = max(mx, 4 * 256 * blk)
-        T = max_prefill_tokens
-        tp = min(c.tp for c in cfgs)
-        act = T * (2 * a.hidden + a.qkv_dim // tp + a.num_query_heads * a.head_dim // tp + a.ffn // tp) * 2
-        act += 2 * T * (-(-a.hidden // 64)) * 4 + 2 * T * 4 * (a.vocab // tp) // max(T // 512, 1)
-        ws = 2 * self.GEMM_WS_BYTES + 3 * T * a.hidden * 2
-        return int(mx + act + ws + (2 << 30))
+        run (ADVICE: the pool must leave room for it); see :func:`runtime_reserve`."""
+        return runtime_reserve(self.arch, self.gpu, cfg_p, cfg_d, max_prefill_tokens, self.block_size,
+                               self.GEMM_WS_BYTES, self.RESHARD_CHUNK_BYTES)["total"]
 
     def check_peer_errors(self) -> None:
         """Raise if a fused TP combine's peer barrier timed out (host sync)."""
@@ -1004,7 +1078,7 @@ class Worker:
         ar = self._arena(B) if st.tp_comm.size > 1 else None
         self._graph_capacity(B)
         key = (B, tables.shape[1], st.cfg, self.pool.data_ptr(), st.arena.data_ptr(),
-               ar.generation if ar is not None else 0, self.fold_norm,
+               ar.generation if ar is not None else 0, self.fold_norm, self.tp_fold,
                self.fuse_rope, self.split_k)
         ent = self._graphs.get(key)
         if ent is None:
@@ -1100,6 +1174,7 @@ class Worker:
         nq, nk = st.weights.n_q_heads, st.weights.n_kv_heads
         lanes = []
         ar = self._arena(spans[0][1] - spans[0][0]) if len(spans) == 1 else None
+        fold = self._tp_fold(ar)
         final = st.stage == st.cfg.pp - 1
         for li, ((b0, b1), s) in enumerate(zip(spans, streams)):
             with torch.cuda.stream(s):
@@ -1111,7 +1186,10 @@ class Worker:
                 if ar is not None:
                     x = ar.x[:n]
                     ops.embedding(v["tok"], self.w("embed"), st.weights.vocab_begin, ar.part[:n])
-                    ar.combine(n, self.w(f"L{st.weights.layer_begin}.attn_norm"), a.rms_eps)
+                    if fold:
+                        ar.combine_ss(n)
+                    else:
+                        ar.combine(n, self.w(f"L{st.weights.layer_begin}.attn_norm"), a.rms_eps)
                     v["h_ready"] = True
                 else:
                     x = buf.get("x")
@@ -1130,12 +1208,16 @@ class Worker:
             for s, x, attn, buf, v in lanes:
                 with torch.cuda.stream(s):
                     v["h_ready"] = self._block(x, layer, attn, buf, (v["pos"], v["slot"]), cap, ar=ar,
-                                               h_ready=v["h_ready"], final=final)
+                                               h_ready=v["h_ready"], final=final, fold=fold)
         for s, x, _, buf, v in lanes:
             with torch.cuda.stream(s):
                 rn = None
-                if ar is not None and v["h_ready"]:
-                    h = ar.h[: x.shape[0]]
+                n = x.shape[0]
+                if ar is not None and v["h_ready"] and fold:
+                    h, rn = x, ops.row_norm(ss_in=ar.ss[:n].view(n, 1), ss_in_parts=1, hidden=a.hidden,
+                                            eps=a.rms_eps)
+                elif ar is not None and v["h_ready"]:
+                    h = ar.h[:n]
                 elif self.fold_norm and st.tp_comm.size == 1 and v["h_ready"]:
                     h, rn = x, self._final_rownorm(buf, x.shape[0], int(v["h_ready"]))
                 else:

@@ -23,7 +23,7 @@ import warnings
 
 import torch
 
-from . import ops
+from . import _lib, ops
 from ._lib import SeesawKernelError
 from .comm import Comm
 
@@ -46,11 +46,16 @@ class PeerArena:
         self.sig = torch.zeros(ops.tp_signal_bytes() // 4, dtype=torch.int32, device=device)
         # the LM head's argmax keys of every row (vocab-parallel greedy token)
         self.keys = torch.zeros(rows, dtype=torch.int64, device=device)
+        # folded-norm layout: per-row fp32 sum of squares of x (instead of h)
+        self.ss = torch.zeros(max(rows, 4), dtype=torch.float32, device=device)
         self.err = torch.zeros(1, dtype=torch.int32, device=device)
         torch.cuda.current_stream(device).synchronize()
         self._maps: list = []  # peer mappings live exactly as long as the arena
         self.addrs = {k: comm.peer_addresses(getattr(self, k), self._maps)
-                      for k in ("part", "x", "h", "sig", "keys")}
+                      for k in ("part", "x", "h", "sig", "keys", "ss")}
+        # the address tables as ctypes arrays, built once (a combine is
+        # launched twice per layer)
+        self._arrays = {k: _lib.uint64_array(v) for k, v in self.addrs.items()}
         self.usable = self._self_test()
 
     def combine(self, rows: int, gamma: torch.Tensor | None, eps: float) -> None:
@@ -62,6 +67,14 @@ class PeerArena:
         a = self.addrs
         ops.tp_allreduce_rmsnorm(a["part"], a["x"], a["h"] if gamma is not None else None, a["sig"],
                                  self.comm.rank, rows, self.hidden, gamma, eps, 0, self.max_blocks, self.err)
+
+    def combine_ss(self, rows: int) -> None:
+        """x[:rows] <- sum over ranks of part[:rows] and ss[:rows] <- the
+        rows' sums of squares, on every rank (the folded-norm combine: the
+        consumer GEMMs scale their rows by 1/rms from ss)."""
+        a = self._arrays
+        ops.tp_allreduce_rowss(a["part"], a["x"], a["ss"], a["sig"], self.comm.rank, rows, self.hidden, 0,
+                               self.max_blocks, self.err)
 
     def argmax(self, rows: int, out_idx: torch.Tensor) -> None:
         """out_idx[:rows] <- greedy token of every row from the ranks' LM-head
@@ -108,8 +121,16 @@ class PeerArena:
         # wait with the GIL released: virtual ranks (threads) must still be
         # able to launch their half of the barrier while this one waits
         torch.cuda.current_stream(dev).synchronize()
-        ok = (int(self.err.item()) == 0 and torch.equal(self.x[:rows], want) and torch.equal(self.h[:rows], ref_h)
-              and torch.equal(got_idx, want_idx))
+        ok_h = torch.equal(self.x[:rows], want) and torch.equal(self.h[:rows], ref_h)
+        # the folded-norm variant: same x, and the rows' sums of squares
+        self.x[:rows].zero_()
+        self.combine_ss(rows)
+        torch.cuda.current_stream(dev).synchronize()
+        wf = want.float()
+        ss_ref = (wf * wf).sum(-1)
+        ok_ss = torch.equal(self.x[:rows], want) and bool(
+            torch.allclose(self.ss[:rows], ss_ref, rtol=1e-5, atol=1e-6))
+        ok = int(self.err.item()) == 0 and ok_h and ok_ss and torch.equal(got_idx, want_idx)
         flags = torch.tensor([1.0 if ok else 0.0], device=dev)
         self.comm.all_reduce_(flags)  # every member agrees on the outcome
         good = int(flags.item()) == n

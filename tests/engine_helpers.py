@@ -72,7 +72,7 @@ def step_logits(worker) -> dict:
 
 
 def greedy_margins(arch, reqs, prompts, outputs, tp_prefill, tp_decode, max_pos=256, pp_prefill=1,
-                   fold_norm=True, weights=None, gpu_logits=None, pp_decode=1):
+                   fold_norm=True, weights=None, gpu_logits=None, pp_decode=1, tp_fold=False):
     """Teacher-forced comparison with the bf16-faithful oracle: per step
     (seq, step, gpu token, oracle token, oracle top-1/top-2 margin, measured
     max |gpu - oracle| logit deviation or None).  ``fold_norm`` mirrors the
@@ -80,7 +80,7 @@ def greedy_margins(arch, reqs, prompts, outputs, tp_prefill, tp_decode, max_pos=
     ``pp_prefill`` places the stage boundaries."""
     oracle = lo.LlamaOracle(oracle_arch(arch), seed=0, bf16_faithful=True, max_pos=max_pos,
                             tp_prefill=tp_prefill, tp_decode=tp_decode, fold_norm=fold_norm, pp_prefill=pp_prefill,
-                            weights=weights, pp_decode=pp_decode)
+                            weights=weights, pp_decode=pp_decode, tp_fold=tp_fold)
     rows = []
     for r, p in zip(reqs, prompts):
         got = outputs[r.id]
@@ -107,13 +107,13 @@ TIE_EPS = 0.02
 
 
 def check_greedy(arch, reqs, prompts, outputs, tp_prefill, tp_decode, max_pos=256, pp_prefill=1,
-                 fold_norm=True, gpu_logits=None, max_subs=None, weights=None, pp_decode=1):
+                 fold_norm=True, gpu_logits=None, max_subs=None, weights=None, pp_decode=1, tp_fold=False):
     """Greedy identity against the bf16-faithful oracle (teacher forced).
     ``gpu_logits``: step_logits() of the run.  Returns {"steps",
     "substitutions": [(seq, step, gpu, oracle, margin, deviation)],
     "min_margin", "deviations"}."""
     rows = greedy_margins(arch, reqs, prompts, outputs, tp_prefill, tp_decode, max_pos, pp_prefill, fold_norm,
-                          weights, gpu_logits, pp_decode)
+                          weights, gpu_logits, pp_decode, tp_fold)
     subs = [r for r in rows if r[2] != r[3]]
     for sid, k, g, e, margin, dev in subs:
         bound = TIE_EPS if dev is None else dev

@@ -220,3 +220,45 @@ def test_gemm_tail_split(cuda, mode, M, N, K, bn, splits):
         sref = torch.nn.functional.silu(a.float() @ wv[:, 0].reshape(F, K).float().T) * (
             a.float() @ wv[:, 1].reshape(F, K).float().T)
         assert (s.float() - sref).abs().max().item() < 3e-2 * sref.abs().max().item() + 1e-2
+
+
+@pytest.mark.parametrize("mode", ["single", "2sm"])
+@pytest.mark.parametrize("M,N,K,bn", [(512, 4096, 4096, 256), (512, 6144, 4096, 256), (512, 4096, 14336, 256),
+                                      (512, 28672, 4096, 256), (300, 640, 1000, 192), (129, 448, 2048, 224),
+                                      (512, 16032, 4096, 128), (64, 256, 4096, 128), (1000, 3000, 704, 256)])
+def test_gemm_stream_k(cuda, mode, M, N, K, bn):
+    """Stream-K (forced): whole tiles, then the last rounds' k-blocks split
+    evenly over the persistent CTAs, shared tiles reduced in k order by their
+    last contributor into TMEM -- every epilogue, deterministic, counters
+    left zero."""
+    from paper_2503_06433_b200._lib import SSB_GEMM_2SM, SSB_GEMM_STREAMK
+
+    flag = bn | SSB_GEMM_STREAMK | (SSB_GEMM_2SM if mode == "2sm" else 0)
+    g = torch.Generator(device="cuda").manual_seed(M * 3 + N + K)
+    a = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device=cuda, generator=g) / K**0.5).to(torch.bfloat16)
+    ws = _ws(cuda)
+    out = ops.gemm(a, w, block_n=flag, workspace=ws)
+    outs = [ops.gemm(a, w, block_n=flag, workspace=ws) for _ in range(3)]
+    torch.cuda.synchronize()
+    ref = _ref(a, w)
+    assert (out.float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item() + 1e-2
+    assert all(torch.equal(out, o) for o in outs), "stream-K reduction must be deterministic"
+    assert int(ws[: 64 << 10].view(torch.int32).abs().sum()) == 0
+    f = ops.gemm(a, w, out_f32=True, block_n=flag, workspace=ws)
+    r = torch.randn(M, N, device=cuda, generator=g).to(torch.bfloat16)
+    exp = ref + r.float()
+    ops.gemm(a, w, out=r, residual=r, block_n=flag, workspace=ws)
+    torch.cuda.synchronize()
+    assert (f - ref).abs().max().item() <= 1e-3 * ref.abs().max().item() + 1e-3
+    assert (r.float() - exp).abs().max().item() <= 2e-2 * exp.abs().max().item() + 2e-2
+    if bn % 64 == 0 and N % 64 == 0:
+        F = N // 2
+        s = ops.gemm(a, w, silu_mul=True, block_n=flag, workspace=ws)
+        torch.cuda.synchronize()
+        wv = w.view(F // 32, 2, 32, K)
+        gg = a.float() @ wv[:, 0].reshape(F, K).float().T
+        uu = a.float() @ wv[:, 1].reshape(F, K).float().T
+        sref = torch.nn.functional.silu(gg) * uu
+        assert (s.float() - sref).abs().max().item() < 3e-2 * sref.abs().max().item() + 1e-2
+    assert int(ws[: 64 << 10].view(torch.int32).abs().sum()) == 0

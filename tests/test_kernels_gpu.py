@@ -92,17 +92,18 @@ def test_rope_and_paged_append(cuda):
         assert torch.equal(P[b, 2, 1, :, o], qkv.view(T, -1, d)[t, nq + nk :])
 
 
-@pytest.mark.parametrize("flag", ["auto", "b128", "b256_2sm", "split3", "split3_2sm"])
+@pytest.mark.parametrize("flag", ["auto", "b128", "b256_2sm", "split3", "split3_2sm", "sk128", "sk256_2sm"])
 @pytest.mark.parametrize("M,nq,nk,K,neg", [(300, 8, 2, 512, False), (512, 32, 8, 4096, False),
                                            (129, 4, 1, 1024, True), (64, 32, 8, 256, True)])
 def test_qkv_gemm_rope_kv_fused_bit_exact(cuda, M, nq, nk, K, neg, flag):
     """The QKV GEMM with RoPE + paged K/V append in its epilogue equals the
     unfused gemm -> rope_kv_append pair bit for bit (qkv buffer and pool),
     for every tile/cluster/split configuration."""
-    from paper_2503_06433_b200._lib import SSB_GEMM_2SM, SSB_GEMM_SPLIT_SHIFT
+    from paper_2503_06433_b200._lib import SSB_GEMM_2SM, SSB_GEMM_SPLIT_SHIFT, SSB_GEMM_STREAMK as SK
 
     bn = {"auto": 0, "b128": 128, "b256_2sm": 256 | SSB_GEMM_2SM, "split3": 128 | (3 << SSB_GEMM_SPLIT_SHIFT),
-          "split3_2sm": 256 | SSB_GEMM_2SM | (3 << SSB_GEMM_SPLIT_SHIFT)}[flag]
+          "split3_2sm": 256 | SSB_GEMM_2SM | (3 << SSB_GEMM_SPLIT_SHIFT), "sk128": 128 | SK,
+          "sk256_2sm": 256 | SSB_GEMM_2SM | SK}[flag]
     arch = PRESETS["llama3-8b"]
     d = 128
     cos, sin = rope_tables(arch, 2048)
@@ -124,11 +125,12 @@ def test_qkv_gemm_rope_kv_fused_bit_exact(cuda, M, nq, nk, K, neg, flag):
     if flag == "auto":  # the unfused reference runs the plan the fused launch picks (same fp32 sums)
         from paper_2503_06433_b200._lib import SSB_EPI_ROPE_KV
 
-        from paper_2503_06433_b200._lib import SSB_GEMM_TAIL
+        from paper_2503_06433_b200._lib import SSB_GEMM_STREAMK, SSB_GEMM_TAIL
 
         (mode, pbn, sp), _ = ops.gemm_plan(M, w.shape[0], K, SSB_EPI_ROPE_KV, 0, ws.numel())
         ref_bn = pbn | (SSB_GEMM_2SM if mode == 2 else 0) | (abs(sp) << SSB_GEMM_SPLIT_SHIFT if abs(sp) > 1 else 0)
         ref_bn |= SSB_GEMM_TAIL if sp < 0 else 0
+        ref_bn |= SSB_GEMM_STREAMK if sp == 0 else 0
     else:
         ref_bn = bn
     ref = ops.gemm(a, w, workspace=ws, block_n=ref_bn)

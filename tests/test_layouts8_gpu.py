@@ -69,6 +69,7 @@ def _run(arch, cfg_p, cfg_d, reqs, prompts, gpu_memory=4e9, fused_tp=False, snap
         with torch.cuda.stream(torch.cuda.Stream(dev) if fused_tp else torch.cuda.current_stream(dev)):
             wk = Worker(arch, comms[r], cfg_p.dp, dev, seed=0, max_pos=512)
             wk.fused_tp = fused_tp
+            wk.tp_fold = False  # the fused combine's bit-identity with the all-reduce path
 
             def before(w, blocks, cfg_to):
                 snaps[(r, "pool_before")] = (w.pool.detach().cpu().clone(), blocks.copy())

@@ -108,4 +108,8 @@ def test_two_process_pp2_tp2(cuda, tiered, p2p, fused_tp):
     assert res[0]["outputs"] == res[1]["outputs"]
     arch = PRESETS["tiny"]
     reqs = [Request(i, 64, 32) for i in range(8)]
-    check_greedy(arch, reqs, synthetic_prompts(reqs, arch.vocab), res[0]["outputs"], 1, 2, pp_prefill=2)
+    # the fused decode combine runs with the folded norm (SSB_TP_FOLD=1)
+    # (the folded norm moves h's bf16 rounding into the fp32 accumulator:
+    # genuine ties, margins < 0.02, may flip on up to 2 % of the steps)
+    check_greedy(arch, reqs, synthetic_prompts(reqs, arch.vocab), res[0]["outputs"], 1, 2, pp_prefill=2,
+                 tp_fold=fused_tp, max_subs=(len(reqs) * 32) // 50 if fused_tp else None)

@@ -88,13 +88,17 @@ if __name__ == "__main__":
 
 def bench_splitk():
     """Forced (mode, bn, splits) sweep vs the auto plan on decode shapes."""
-    from paper_2503_06433_b200._lib import SSB_GEMM_2SM, SSB_GEMM_SPLIT_SHIFT, SSB_GEMM_TAIL
+    from paper_2503_06433_b200._lib import SSB_GEMM_2SM, SSB_GEMM_SPLIT_SHIFT, SSB_GEMM_STREAMK, SSB_GEMM_TAIL
+
+    only = os.environ.get("SSB_SWEEP_SHAPES")  # "M,N,K;M,N,K" restricts the sweep
 
     ws = torch.zeros(256 << 20, dtype=torch.uint8, device="cuda")
     shapes = [(M, N, K) for M in (512, 256) for N, K in
               ((6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336), (128256, 4096), (768, 4096), (4096, 512),
                (3584, 4096), (4096, 1792), (16032, 4096))]
     shapes += [(16384, 6144, 4096), (16384, 4096, 14336), (2048, 4096, 4096)]
+    if only:
+        shapes = [tuple(int(x) for x in sh.split(",")) for sh in only.split(";")]
     for M, N, K in shapes:
         a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
         w = (torch.randn(N, K, device="cuda") / K**0.5).to(torch.bfloat16)
@@ -119,6 +123,13 @@ def bench_splitk():
                         except Exception as e:  # noqa: BLE001
                             continue
                         res.append((f"m{mode}b{bn}s{sp}" + ("t" if tail else ""), None, ms))
+                if M <= 2048:
+                    flag = bn | SSB_GEMM_STREAMK | (SSB_GEMM_2SM if mode == 2 else 0)
+                    try:
+                        ms = timed(lambda: ops.gemm(a, w, out=c, block_n=flag, workspace=ws), iters=10)
+                        res.append((f"m{mode}b{bn}sk", None, ms))
+                    except Exception:  # noqa: BLE001
+                        pass
         best = min(res[2:], key=lambda r: r[2])
         print(json.dumps({"M": M, "N": N, "K": K, "auto_plan": res[0][1], "auto_ms": res[0][2],
                           "auto_tflops": fl / res[0][2] / 1e9, "cublas_ms": ms_t, "cublas_tflops": fl / ms_t / 1e9,
