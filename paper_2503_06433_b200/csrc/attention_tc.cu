@@ -667,8 +667,20 @@ constexpr int kPairKSt = 3, kPairVSt = 2;
 // pair i's second exponential by polynomial when (i & kPolyMask): 0 = off.
 // Measured: 1-in-4 on the FMA pipe is 5 % SLOWER (the softmax is issue- not
 // MUFU-bound at 2 warps per SMSP), so every exponential uses ex2.approx.
-constexpr int kPolyMask = 0;
-constexpr int kThreadsPair = 320;
+// (template parameter POLY of the pair kernel; SSB_ATTN_POLY selects 1 or 3
+// for the A/B, 0 by default)
+// 3 warpgroups: WG0 = TMA (warp 0) + MMA issue (warp 1) + 2 idle warps,
+// WG1 / WG2 = softmax of head A / B (one thread per query row).  Registers
+// are re-balanced per warpgroup (setmaxnreg): WG0 drops to 80, the softmax
+// warpgroups rise to 208 and nothing spills.  The increase draws on the
+// registers the CTA was launched with (384 x 168), so 128 x 80 + 256 x 208
+// must not exceed them -- a larger request blocks setmaxnreg.inc forever -- with the 168 the 320-thread layout had uniformly, the
+// softmax kept loop state in local memory (ncu: LDL on the S-wait ->
+// tcgen05.ld path and in the O epilogue, ~9 % of the warps' stall samples).
+constexpr int kThreadsPair = 384;
+constexpr int kRegsPairCtl = 80, kRegsPairSoftmax = 208;
+static_assert(128 * kRegsPairCtl + 256 * kRegsPairSoftmax <= kThreadsPair * 168,
+              "setmaxnreg.inc would wait for registers the CTA does not own");
 
 struct SmemPair {
   static constexpr int kQ = 0;                          // Q_A, Q_B
@@ -745,6 +757,7 @@ struct PairIter {
   }
 };
 
+template <int kPolyMask>
 __global__ void __launch_bounds__(kThreadsPair, 1)
     prefill_attn_tc_pair(const __grid_constant__ CUtensorMap tmap, const int32_t* __restrict__ cu, int nseq,
                          int n_qt_max, int nq, int nk, __nv_bfloat16* __restrict__ out, int ldo, float scale_log2) {
@@ -797,7 +810,9 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
   // columns: S/P of head h at 128 h, O of head h at 256 + 128 h
   auto t_s = [&](int head) { return tmem + 128u * head; };
   auto t_o = [&](int head) { return tmem + 256u + 128u * head; };
-
+  if (warp < 4) {
+  // ---------------- WG0: TMA producer (warp 0), MMA issuer (warp 1) ----------------
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsPairCtl));
   if (warp == 0) {
     // lane 0: Q_A, Q_B and K tiles; lane 1: V tiles
     if (lane < 2) {
@@ -886,9 +901,11 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
         ++ic;
       }
     }
+  }
   } else {
     // ---------------- softmax: warpgroup hh = head, thread = query row ----------------
-    const int hh = (warp - 2) >> 2;
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsPairSoftmax));
+    const int hh = (warp - 4) >> 2;
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
@@ -981,15 +998,16 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
       tc_fence_after();
       const float inv = l > 0.f ? __frcp_rn(l) : 0.f;
       __nv_bfloat16* orow = out + static_cast<size_t>(start + qrow) * ldo + (2 * pair + hh) * kD;
-#pragma unroll 1
-      for (int c = 0; c < kD / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(o_acc + c * 32, v);
+      {
+        // the whole O row: four 32-column loads in flight, one wait
+        uint32_t v[kD];
+#pragma unroll
+        for (int c = 0; c < kD / 32; ++c) tmem_ld32(o_acc + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + c * 32));
         tmem_ld_wait();
         if (qrow < len) {
-          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+          uint4* dst = reinterpret_cast<uint4*>(orow);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < kD / 8; ++q) {
             uint4 o;
             o.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]) * inv, __uint_as_float(v[8 * q + 1]) * inv);
             o.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv);
@@ -1026,17 +1044,21 @@ int launch_prefill_attn_tc(const void* qkv, int ld, int T, int nq, int nk, const
     return e ? atoi(e) : 0;
   }();
   if (persistent && (nq / nk) % 2 == 0 && !force_single) {
+    static const int poly = [] {
+      const char* e = getenv("SSB_ATTN_POLY");  // A/B: exponentials emulated on the FMA pipe
+      return e ? atoi(e) : 0;
+    }();
+    auto kern = poly == 3 ? prefill_attn_tc_pair<3> : poly == 1 ? prefill_attn_tc_pair<1> : prefill_attn_tc_pair<0>;
     static bool pair_attr = false;
     if (!pair_attr) {
-      SSB_CUDA(cudaFuncSetAttribute(prefill_attn_tc_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    SmemPair::kBytes));
+      SSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemPair::kBytes));
       pair_attr = true;
     }
     const int n_qt = (max_len + kT - 1) / kT;
     const long items = static_cast<long>(n_qt) * (nq / 2) * nseq;
     const int grid = static_cast<int>(std::min<long>(num_sms(), items));
-    prefill_attn_tc_pair<<<grid, kThreadsPair, SmemPair::kBytes, s>>>(
-        map, cu, nseq, n_qt, nq, nk, static_cast<__nv_bfloat16*>(out), ldo, scale * 1.4426950408889634f);
+    kern<<<grid, kThreadsPair, SmemPair::kBytes, s>>>(map, cu, nseq, n_qt, nq, nk, static_cast<__nv_bfloat16*>(out),
+                                                     ldo, scale * 1.4426950408889634f);
     return check_launch("prefill_attn_tc_pair");
   }
   if (persistent) {

@@ -1060,6 +1060,14 @@ class Worker:
         st = self.state
         if st.cfg.pp != 1:
             return False
+        from .comm import ThreadComm
+
+        if isinstance(self.world, ThreadComm) and self.world.size > st.tp_comm.size:
+            # virtual ranks of OTHER replicas share this device and process and
+            # step on their own schedule: their device-wide synchronisations
+            # would invalidate this thread's capture (one process per GPU has
+            # no such neighbours)
+            return False
         if st.tp_comm.size > 1:
             return self.fuse_argmax and self._arena(B) is not None
         return True

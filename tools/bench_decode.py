@@ -4,6 +4,7 @@ decode-lane overlap settings.  Pool contents are random (timing only)."""
 from __future__ import annotations
 
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -43,11 +44,13 @@ def main(configs):
         e.record()
         torch.cuda.synchronize()
         ms = s.elapsed_time(e) / steps
-        out.append({"lanes": lanes, "cap": cap, "ms_per_step": ms})
+        out.append({"lanes": lanes, "cap": cap, "ms_per_step": ms,
+                    "env": {k: v for k, v in os.environ.items() if k.startswith("SSB_")}})
         print(json.dumps(out[-1]), flush=True)
     return out
 
 
 if __name__ == "__main__":
-    cfgs = [(1, 0), (2, 0), (2, 132), (2, 120), (2, 108), (2, 96)]
+    # --ab: the default single-lane step only (A/B of SSB_* switches across runs)
+    cfgs = [(1, 0)] if "--ab" in sys.argv else [(1, 0), (2, 0), (2, 132), (2, 120), (2, 108), (2, 96)]
     main(cfgs)

@@ -67,10 +67,11 @@ if __name__ == "__main__":
             cu = torch.tensor(np.concatenate([[0], np.cumsum(lens)]), dtype=torch.int32, device="cuda")
             out = torch.empty(T, nq * d, dtype=torch.bfloat16, device="cuda")
             fl = sum(2 * 2 * L * L / 2 * d * nq for L in lens)
-            for v in (0, 2, 1):
+            for v in ((0,) if os.environ.get("SSB_ATTN_ONLY0") else (0, 2, 1)):
                 ms = timed(lambda: ops.prefill_attention(qkv, nq, nk, d, cu, max(lens), out, d ** -0.5, variant=v))
                 print(json.dumps({"lens": f"{len(lens)}x{lens[0]}", "variant": v, "ms": ms,
-                                  "tflops": fl / ms / 1e9}), flush=True)
+                                  "tflops": fl / ms / 1e9, "poly": os.environ.get("SSB_ATTN_POLY", "0")}),
+                      flush=True)
     if args.what == "mc":
         MC1, TWO = 1 << 16, 1 << 18
         shapes = [(8192, 6144, 4096), (8192, 28672, 4096), (8192, 4096, 14336), (512, 6144, 4096),
