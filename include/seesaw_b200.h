@@ -53,6 +53,18 @@ int ssb_device_sm_count(void);
  * rank's early-resident GEMM could hold the SMs its peer's producer needs). */
 int ssb_set_pdl(int on);
 
+/* CUDA IPC peer mapping for the peer-memory kernels (fused TP combine, peer
+ * argmax, p2p KV re-shard): export names the cudaMalloc allocation holding
+ * `ptr` (64-byte cudaIpcMemHandle_t) and ptr's offset in it; open maps a peer
+ * process's handle in THIS process's context of `device` -- the GPU whose kernels will
+ * dereference the pointer -- with peer access enabled on open; close it when
+ * the buffer it maps is released.  (Mapping it under the exporter's device
+ * instead would leave the local GPU without peer access to it.)
+ * Boundary for the reference's ReshardPlan transfers, reshard.py:125-201. */
+int ssb_ipc_export(const void* ptr, void* handle_out /* 64 bytes */, int64_t* offset_out);
+int ssb_ipc_open(const void* handle, int device, void** out_ptr);
+int ssb_ipc_close(void* ptr, int device);
+
 /* ------------------------------------------------------------------------
  * Dense projections (bf16 tcgen05/TMEM GEMM fed by TMA).
  * Replaces perf.py:59-65 (linear weight traffic) and perf.py:92-111 (linear

@@ -7,10 +7,12 @@ The product path has no fallback: if the library is missing or a call fails,
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libseesaw_b200.so"
+# SSB_LIB: an A/B build of the same library (tools/build_ab_lib.py)
+LIB_PATH = Path(os.environ.get("SSB_LIB") or Path(__file__).resolve().parent / "libseesaw_b200.so").resolve()
 
 SSB_EPI_NONE = 0
 SSB_EPI_RESIDUAL = 1
@@ -125,6 +127,12 @@ def load() -> ctypes.CDLL:
             lib.ssb_device_sm_count.restype = ctypes.c_int
             lib.ssb_set_pdl.restype = ctypes.c_int
             lib.ssb_set_pdl.argtypes = [_I]
+            lib.ssb_ipc_export.restype = ctypes.c_int
+            lib.ssb_ipc_export.argtypes = [_P, _P, ctypes.POINTER(ctypes.c_int64)]
+            lib.ssb_ipc_open.restype = ctypes.c_int
+            lib.ssb_ipc_open.argtypes = [_P, _I, ctypes.POINTER(ctypes.c_void_p)]
+            lib.ssb_ipc_close.restype = ctypes.c_int
+            lib.ssb_ipc_close.argtypes = [_P, _I]
             lib.ssb_gemm_plan.restype = ctypes.c_int64
             lib.ssb_gemm_plan.argtypes = [_I, _I, _I, _I, _I, _I64, _PI32]
             lib.ssb_tp_signal_bytes.restype = ctypes.c_size_t

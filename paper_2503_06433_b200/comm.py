@@ -199,23 +199,83 @@ class TorchComm(Comm):
 
 
     def peer_addresses(self, t: torch.Tensor, keep: list) -> list[int]:
-        """CUDA IPC: every member exports its allocation, the others map it
-        (cudaIpcOpenMemHandle through torch's shared-storage path); the
-        mapped peer storages go to ``keep``."""
-        storage = t.untyped_storage()
-        handle = storage._share_cuda_()
-        mine = (handle, t.storage_offset() * t.element_size())
+        """CUDA IPC: every member exports the cudaMalloc allocation holding
+        ``t`` (handle + offset, ssb_ipc_export), the others map it in the
+        context of THEIR OWN device (ssb_ipc_open, peer access enabled on
+        open), so their kernels can dereference it over NVLink.  (torch's
+        shared-storage path would map it under the exporter's device index:
+        a context on the peer GPU, and no peer access for the local one.)
+        The mappings go to ``keep``; each is closed when the last holder of
+        its allocation drops it."""
+        import ctypes
+
+        from . import _lib
+
+        lib = _lib.load()
+        handle = ctypes.create_string_buffer(64)
+        off = ctypes.c_int64(0)
+        rc = lib.ssb_ipc_export(ctypes.c_void_p(t.data_ptr()), handle, ctypes.byref(off))
+        if rc != 0:
+            raise _lib.SeesawKernelError(f"ssb_ipc_export failed ({rc}): {lib.ssb_last_error().decode()}")
+        mine = (bytes(handle.raw), int(off.value))
         objs: list = [None] * self.size
         self._dist.all_gather_object(objs, mine, group=self.group)
+        dev = t.device.index if t.device.index is not None else torch.cuda.current_device()
         addrs = []
-        for r, (h, off) in enumerate(objs):
+        for r, (h, o) in enumerate(objs):
             if r == self.rank:
                 addrs.append(t.data_ptr())
                 continue
-            peer = torch.UntypedStorage._new_shared_cuda(*h)
-            keep.append(peer)
-            addrs.append(peer.data_ptr() + off)
+            m = _IpcMapping.open(h, dev)
+            keep.append(m)
+            addrs.append(m.base + o)
         return addrs
+
+
+class _IpcMapping:
+    """A peer allocation mapped into this process (one cudaIpcOpenMemHandle
+    per (handle, device), shared by every buffer carved from it; closed with
+    its last holder)."""
+
+    _open: dict = {}
+    _lock = threading.Lock()
+
+    def __init__(self, key, base: int) -> None:
+        self.key, self.base = key, base
+
+    @classmethod
+    def open(cls, handle: bytes, device: int) -> "_IpcMapping":
+        import ctypes
+
+        from . import _lib
+
+        key = (handle, device)
+        with cls._lock:
+            ent = cls._open.get(key)
+            if ent is None:
+                lib = _lib.load()
+                ptr = ctypes.c_void_p(0)
+                rc = lib.ssb_ipc_open(handle, device, ctypes.byref(ptr))
+                if rc != 0:
+                    raise _lib.SeesawKernelError(f"ssb_ipc_open failed ({rc}): {lib.ssb_last_error().decode()}")
+                ent = cls._open[key] = [int(ptr.value), 0]
+            ent[1] += 1
+            return cls(key, ent[0])
+
+    def __del__(self) -> None:
+        try:
+            with self._lock:
+                ent = self._open.get(self.key)
+                if ent is None:
+                    return
+                ent[1] -= 1
+                if ent[1] == 0:
+                    del self._open[self.key]
+                    from . import _lib
+
+                    _lib.load().ssb_ipc_close(ent[0], self.key[1])
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
 
 
 _GROUPS: dict[tuple[int, ...], object] = {}

@@ -106,6 +106,70 @@ int ssb_set_pdl(int on) {
   return prev;
 }
 
+int ssb_ipc_export(const void* ptr, void* handle_out, int64_t* offset_out) {
+  using namespace ssb;
+  SSB_REQUIRE(ptr && handle_out && offset_out, "ssb_ipc_export: null argument");
+  // the cudaMalloc allocation holding ptr (a caching allocator hands out
+  // interior pointers): its base is what the handle names
+  static PFN_cuMemGetAddressRange_v3020 range = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+  });
+  if (!range) {
+    set_error("ssb_ipc_export: cuMemGetAddressRange entry point unavailable");
+    return SSB_EUNSUPPORTED;
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS) {
+    set_error("ssb_ipc_export: cuMemGetAddressRange failed for %p", ptr);
+    return SSB_EARG;
+  }
+  cudaIpcMemHandle_t h;
+  SSB_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  memcpy(handle_out, &h, sizeof(h));
+  *offset_out = static_cast<int64_t>(reinterpret_cast<uintptr_t>(ptr) - static_cast<uintptr_t>(base));
+  return 0;
+}
+
+int ssb_ipc_open(const void* handle, int device, void** out_ptr) {
+  using namespace ssb;
+  SSB_REQUIRE(handle && out_ptr, "ssb_ipc_open: null argument");
+  int prev = 0;
+  SSB_CUDA(cudaGetDevice(&prev));
+  SSB_CUDA(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  const cudaError_t e = cudaIpcOpenMemHandle(out_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error("ssb_ipc_open: cudaIpcOpenMemHandle on device %d: %s", device, cudaGetErrorString(e));
+    return static_cast<int>(e);
+  }
+  return 0;
+}
+
+int ssb_ipc_close(void* ptr, int device) {
+  using namespace ssb;
+  int prev = 0;
+  SSB_CUDA(cudaGetDevice(&prev));
+  SSB_CUDA(cudaSetDevice(device));
+  const cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error("ssb_ipc_close: %s", cudaGetErrorString(e));
+    return static_cast<int>(e);
+  }
+  return 0;
+}
+
 int ssb_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
                        int64_t height, void* stream) {
   using namespace ssb;

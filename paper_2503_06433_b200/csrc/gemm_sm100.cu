@@ -113,13 +113,6 @@ struct Params {
   int sk_dp_rounds;
   int sk_tile0;
   long long sk_W;
-  // PDL weight prefetch: B (the weight matrix, never written by the kernels
-  // of a PDL chain) of the first unit's first stages is loaded BEFORE
-  // griddepcontrol.wait, so its HBM latency overlaps the predecessor's tail
-  int prefetch_b;
-  // epilogue operands (residual chunks, RoPE position / slot / tables)
-  // loaded before the accumulator wait (A/B switch SSB_GEMM_EPI_PREFETCH)
-  int epi_prefetch;
 };
 
 // Grouped rasterisation: kGroupM tiles of the "band" dimension share one
@@ -267,20 +260,7 @@ __device__ __forceinline__ float sq_bf16x2(uint32_t v, float ss) {
 
 // Final epilogue of 32 accumulator columns [col, col+32) of one row; `ss`
 // accumulates the squares of the stored bf16 values when p.ss_out is set.
-// The residual row segment of a 32-column chunk (16-byte loads), issued
-// ahead of its use so its latency overlaps the MMAs / the previous chunk.
-__device__ __forceinline__ void load_resid(const Params& p, int row, int col, uint4 (&r)[4]) {
-  if (col + 32 <= p.N) {
-    const uint4* src =
-        reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.R) + static_cast<size_t>(row) * p.ldr + col);
-#pragma unroll
-    for (int v = 0; v < 4; ++v) r[v] = src[v];
-  }
-}
-
-// `pre`: the chunk's residual, already loaded by load_resid (else read here).
-__device__ __forceinline__ void store_cols(const Params& p, int row, int col, float (&f)[32], float& ss,
-                                           const uint4 (*pre)[4] = nullptr) {
+__device__ __forceinline__ void store_cols(const Params& p, int row, int col, float (&f)[32], float& ss) {
   __nv_bfloat16* crow = reinterpret_cast<__nv_bfloat16*>(p.C) + static_cast<size_t>(row) * p.ldc;
   const __nv_bfloat16* rrow =
       p.epi == SSB_EPI_RESIDUAL ? reinterpret_cast<const __nv_bfloat16*>(p.R) + static_cast<size_t>(row) * p.ldr
@@ -301,7 +281,7 @@ __device__ __forceinline__ void store_cols(const Params& p, int row, int col, fl
       const uint4* src = reinterpret_cast<const uint4*>(rrow + col);
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
-        const uint4 r = pre ? (*pre)[v] : src[v];
+        uint4 r = src[v];
         f[8 * v + 0] += bf16_lo(r.x); f[8 * v + 1] += bf16_hi(r.x);
         f[8 * v + 2] += bf16_lo(r.y); f[8 * v + 3] += bf16_hi(r.y);
         f[8 * v + 4] += bf16_lo(r.z); f[8 * v + 5] += bf16_hi(r.z);
@@ -376,27 +356,10 @@ __device__ __forceinline__ void argmax_cols(const Params& p, int col, const floa
   }
 }
 
-// The row's RoPE position and KV slot, and an L1 prefetch of its cos / sin
-// rows: issued while the tile's MMAs run, so the epilogue's per-chunk table
-// reads hit L1 instead of serialising pos -> cos/sin L2 round trips.
-__device__ __forceinline__ void rope_row_prefetch(const Params& p, int row, int& ps, int64_t& slot) {
-  const RopeKV& rk = p.rk;
-  ps = min(max(rk.pos[row], 0), rk.max_pos - 1);
-  slot = rk.slots ? rk.slots[row] : -1;
-  const float* c = rk.cos + static_cast<size_t>(ps) * 64;
-  const float* s = rk.sin + static_cast<size_t>(ps) * 64;
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(c));
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(c + 32));
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(s));
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(s + 32));
-}
-
 // RoPE + KV append of one row's 32-column pair (lo = head columns [i0, i0+32),
 // hi = [i0+64, i0+96)) of head `head`, i0 in {0, 32}.
-// `ps` / `slot`: the row's clamped position and KV slot, loaded once per
-// tile before the accumulator wait (rope_row_prefetch).
 __device__ __forceinline__ void store_rope(const Params& p, int row, int col_lo, const float (&lo)[32],
-                                           const float (&hi)[32], int ps, int64_t slot) {
+                                           const float (&hi)[32]) {
   constexpr int kHd = 128, kHalf = 64;
   const RopeKV& rk = p.rk;
   const int head = col_lo / kHd;
@@ -404,6 +367,7 @@ __device__ __forceinline__ void store_rope(const Params& p, int row, int col_lo,
   __nv_bfloat16* crow = reinterpret_cast<__nv_bfloat16*>(p.C) + static_cast<size_t>(row) * p.ldc;
   uint32_t olo[16], ohi[16];
   if (head < rk.nq + rk.nk) {
+    const int ps = min(max(rk.pos[row], 0), rk.max_pos - 1);
     const float4* cr = reinterpret_cast<const float4*>(rk.cos + static_cast<size_t>(ps) * kHalf + i0);
     const float4* sr = reinterpret_cast<const float4*>(rk.sin + static_cast<size_t>(ps) * kHalf + i0);
 #pragma unroll
@@ -438,6 +402,7 @@ __device__ __forceinline__ void store_rope(const Params& p, int row, int col_lo,
     dhi[v] = make_uint4(ohi[4 * v], ohi[4 * v + 1], ohi[4 * v + 2], ohi[4 * v + 3]);
   }
   if (head >= rk.nq && rk.slots) {
+    const int64_t slot = rk.slots[row];
     if (slot >= 0) {
       const int64_t blk = slot / rk.block_size;
       const int off = static_cast<int>(slot - blk * rk.block_size);
@@ -646,9 +611,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // prefetch) overlapped the previous kernel; from here on global memory the
   // previous kernel writes (A, the residual / output) is touched
   griddep_launch_dependents();
-  // (the producer waits after issuing its weight prefetch, the MMA warp
-  // touches only shared and tensor memory)
-  if (warp >= 2) griddep_wait();
+  if (warp != 1) griddep_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -673,40 +636,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         pol_a = p.group_n ? stream_pol : policy_evict_last();
         pol_b = p.group_n ? policy_evict_last() : stream_pol;
       }
-      // one stage's B tile (arming the stage's full barrier for A and B)
-      auto load_b = [&](int st, int kb, int tn) {
-        if (MODE == 2) {
-          // both CTAs' halves land on the leader's full barrier
-          const uint32_t lbar = mapa_shared(&full[st], 0);
-          if (crank == 0) mbar_arrive_expect_tx(&full[st], 2 * C::kStageBytes);
-          tma_load_2d_cg2(smem_b + st * C::kBBytes, &tmap_b, lbar, kb * kBK, tn * BN + crank * (BN / 2), pol_b);
-        } else {
-          mbar_arrive_expect_tx(&full[st], C::kStageBytes);
-          if (MC == 1)
-            tma_load_2d(smem_b + st * C::kBBytes, &tmap_b, &full[st], kb * kBK, tn * BN, pol_b);
-          else  // my half of the B tile, written into both CTAs of the cluster
-            tma_load_2d_mc(smem_b + st * C::kBBytes + crank * (C::kBBytes / MC), &tmap_b, &full[st], kb * kBK,
-                           tn * BN + crank * (BN / MC), static_cast<uint16_t>((1u << MC) - 1), pol_b);
-        }
-      };
-      auto load_a = [&](int st, int kb, int tm) {
-        if (MODE == 2)
-          tma_load_2d_cg2(smem_a + st * C::kABytes, &tmap_a, mapa_shared(&full[st], 0), kb * kBK, tm * kBM, pol_a);
-        else
-          tma_load_2d(smem_a + st * C::kABytes, &tmap_a, &full[st], kb * kBK, tm * kBM, pol_a);
-      };
-      // weight prefetch: the first unit's first stages of B (every stage is
-      // empty at kernel start), issued before waiting for the predecessor
-      int npre = 0;
-      if (p.prefetch_b && nw > 0) {
-        Work w;
-        get_work<MC>(p, cid, nclusters, 0, crank, w);
-        int um, tn;
-        tile_coords(w.t, units_m, p.tiles_n, p.group_n, p.group_size, um, tn);
-        npre = min(C::kStages, w.kb1 - w.kb0);
-        for (int st = 0; st < npre; ++st) load_b(st, w.kb0 + st, tn);  // unit 0 walks K forwards
-      }
-      griddep_wait();
       int stage = 0;
       uint32_t phase = 0;
       for (int i = 0; i < nw; ++i) {
@@ -717,15 +646,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int tm = um * MC + crank;
         const int kb0 = w.kb0, kb1 = w.kb1;
         const bool rev = p.kserp && (i & 1);
-        for (int j = kb0; j < kb1; ++j) {
+        for (int i = kb0; i < kb1; ++i) {
           // (the MMA warp only counts k-blocks: the order is the producer's)
-          const int kb = rev ? kb1 - 1 - (j - kb0) : j;
-          if (i == 0 && j - kb0 < npre) {
-            load_a(stage, kb, tm);  // B already in flight
+          const int kb = rev ? kb1 - 1 - (i - kb0) : i;
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (MODE == 2) {
+            // both halves land on the leader's full barrier
+            const uint32_t lbar = mapa_shared(&full[stage], 0);
+            if (crank == 0) mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
+            tma_load_2d_cg2(smem_a + stage * C::kABytes, &tmap_a, lbar, kb * kBK, tm * kBM, pol_a);
+            tma_load_2d_cg2(smem_b + stage * C::kBBytes, &tmap_b, lbar, kb * kBK, tn * BN + crank * (BN / 2),
+                            pol_b);
+            if (++stage == C::kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
+          mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+          tma_load_2d(smem_a + stage * C::kABytes, &tmap_a, &full[stage], kb * kBK, tm * kBM,
+                      pol_a);
+          if (MC == 1) {
+            tma_load_2d(smem_b + stage * C::kBBytes, &tmap_b, &full[stage], kb * kBK, tn * BN,
+                        pol_b);
           } else {
-            mbar_wait(&empty[stage], phase ^ 1);
-            load_b(stage, kb, tn);
-            load_a(stage, kb, tm);
+            // my half of the B tile, written into both CTAs of the cluster
+            tma_load_2d_mc(smem_b + stage * C::kBBytes + crank * (C::kBBytes / MC), &tmap_b, &full[stage],
+                           kb * kBK, tn * BN + crank * (BN / MC), static_cast<uint16_t>((1u << MC) - 1), pol_b);
           }
           if (++stage == C::kStages) {
             stage = 0;
@@ -798,19 +745,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool row_ok = row < p.M;
       // the row's 1/rms: loads issued while the tile's MMAs still run
       const float rs = (p.ss_in != nullptr && row_ok) ? row_rms_scale(p, row) : 1.f;
-      // residual epilogue: the first two chunks' residual loads also run
-      // under the MMAs, each later chunk's two chunks ahead of its use (a
-      // dependent residual load per chunk after the accumulator wait was ~0.5
-      // us of exposed L2 latency per chunk on the decode projections)
-      const bool pre_r = p.epi_prefetch && p.epi == SSB_EPI_RESIDUAL && row_ok;
-      uint4 rbuf[2][4];
-      int rope_ps = 0;
-      int64_t rope_slot = -1;
-      if (p.epi_prefetch && p.epi == SSB_EPI_ROPE_KV && row_ok) rope_row_prefetch(p, row, rope_ps, rope_slot);
-      if (pre_r) {
-        load_resid(p, row, tn * BN, rbuf[0]);
-        if (BN > 32) load_resid(p, row, tn * BN + 32, rbuf[1]);
-      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
@@ -834,7 +768,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else if (p.epi == SSB_EPI_ROPE_KV) {
           // per 128-column head: chunk pairs (0, 2) and (1, 3) are the
           // rotate-half partners (i, i + 64)
-          if (!p.epi_prefetch && row_ok) rope_row_prefetch(p, row, rope_ps, rope_slot);
 #pragma unroll 1
           for (int c = 0; c < BN / 32; ++c) {
             if (c & 2) continue;
@@ -852,7 +785,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               scale32(fl, rs);
               scale32(fh, rs);
             }
-            if (row_ok && tn * BN + c * 32 < p.N) store_rope(p, row, tn * BN + c * 32, fl, fh, rope_ps, rope_slot);
+            if (row_ok && tn * BN + c * 32 < p.N) store_rope(p, row, tn * BN + c * 32, fl, fh);
           }
         } else if (p.epi == SSB_EPI_SILU_MUL) {
           // accumulator columns come in (32 gate, 32 up) pairs -> 32 outputs
@@ -875,7 +808,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (row_ok) store_silu(p, row, (tn * BN) / 2 + c * 32, gf, uf);
           }
         } else {
-#pragma unroll
+#pragma unroll 1
           for (int c = 0; c < BN / 32; ++c) {
             uint32_t a[32];
             tmem_ld32(tbase + c * 32, a);
@@ -884,15 +817,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(a[j]);
             if (p.ss_in) scale32(f, rs);
-            if (pre_r) {
-              uint4 cur[4];
-#pragma unroll
-              for (int v = 0; v < 4; ++v) cur[v] = rbuf[c & 1][v];
-              if (c + 2 < BN / 32) load_resid(p, row, tn * BN + (c + 2) * 32, rbuf[c & 1]);
-              store_cols(p, row, tn * BN + c * 32, f, ss, &cur);
-            } else if (row_ok) {
-              store_cols(p, row, tn * BN + c * 32, f, ss);
-            }
+            if (row_ok) store_cols(p, row, tn * BN + c * 32, f, ss);
           }
           if (p.ss_out && row_ok) p.ss_out[static_cast<size_t>(row) * p.tiles_n + tn] = ss;
         }
@@ -1028,12 +953,6 @@ int launch(const void* A, const void* B, void* Cp, const void* R, int M, int N, 
   p.sk = 0;
   p.sk_dp_rounds = p.sk_tile0 = 0;
   p.sk_W = 0;
-  {
-    static const int prefetch_b = gemm_env("SSB_GEMM_PREFETCH_B", 1);
-    p.prefetch_b = prefetch_b;
-    static const int epi_prefetch = gemm_env("SSB_GEMM_EPI_PREFETCH", 1);
-    p.epi_prefetch = epi_prefetch;
-  }
   if (sk) {
     const SKLayout l = sk_layout(unit_tiles, num_kb, groups);
     if (l.on) {

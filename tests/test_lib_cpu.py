@@ -36,8 +36,20 @@ def test_library_exports_every_declared_symbol():
 def test_ctypes_signatures_cover_header():
     declared = set(declared_functions())
     bound = set(_lib.SIGNATURES) | {"ssb_last_error", "ssb_version", "ssb_device_sm_count", "ssb_gemm_plan",
-                                    "ssb_tp_signal_bytes", "ssb_set_pdl"}
+                                    "ssb_tp_signal_bytes", "ssb_set_pdl", "ssb_ipc_export", "ssb_ipc_open",
+                                    "ssb_ipc_close"}
     assert declared == bound
+
+
+def test_ipc_entry_points_reject_null_arguments():
+    """The CUDA IPC mapping calls (comm.TorchComm.peer_addresses) report a
+    null argument as an error code, without touching a device."""
+    lib = _lib.load()
+    out = ctypes.c_void_p(0)
+    assert lib.ssb_ipc_open(None, 0, ctypes.byref(out)) < 0
+    assert b"null" in lib.ssb_last_error()
+    off = ctypes.c_int64(0)
+    assert lib.ssb_ipc_export(None, None, ctypes.byref(off)) < 0
 
 
 def test_argument_errors_are_reported_not_raised():
