@@ -51,11 +51,29 @@ class PeerArena:
         self.err = torch.zeros(1, dtype=torch.int32, device=device)
         torch.cuda.current_stream(device).synchronize()
         self._maps: list = []  # peer mappings live exactly as long as the arena
-        self.addrs = {k: comm.peer_addresses(getattr(self, k), self._maps)
-                      for k in ("part", "x", "h", "sig", "keys", "ss")}
+        self.addrs = {}
+        mapped = True
+        for k in ("part", "x", "h", "sig", "keys", "ss"):
+            try:
+                self.addrs[k] = comm.peer_addresses(getattr(self, k), self._maps)
+            except _lib.SeesawKernelError as exc:  # e.g. no peer access between these GPUs
+                warnings.warn(f"fused TP combine: peer mapping of {k!r} failed on rank {comm.rank} ({exc})",
+                              RuntimeWarning, stacklevel=2)
+                self.addrs[k] = [0] * comm.size
+                mapped = False
+        # every member agrees whether the mappings exist before any kernel
+        # dereferences them (a rank that could not map must not leave its
+        # peers waiting in the self-test's device barrier)
+        flags = torch.tensor([1.0 if mapped else 0.0], device=device)
+        comm.all_reduce_(flags)
         # the address tables as ctypes arrays, built once (a combine is
         # launched twice per layer)
         self._arrays = {k: _lib.uint64_array(v) for k, v in self.addrs.items()}
+        if int(flags.item()) != comm.size:
+            warnings.warn("fused TP combine: peer mappings unavailable on some rank; "
+                          "falling back to all-reduce + rmsnorm", RuntimeWarning, stacklevel=2)
+            self.usable = False
+            return
         self.usable = self._self_test()
 
     def combine(self, rows: int, gamma: torch.Tensor | None, eps: float) -> None:

@@ -95,3 +95,27 @@ def test_missing_peer_times_out_instead_of_hanging(cuda):
             return 0
 
     assert run_threads(2, body)[0] == 1
+
+
+def test_failed_peer_mapping_falls_back_on_every_rank(cuda):
+    """A rank that cannot map a peer buffer (no peer access between two GPUs,
+    an IPC failure) must not leave its peers in the self-test's device
+    barrier: all members agree on the failure first, and every rank ends up
+    with an unusable arena (the caller falls back to all-reduce + rmsnorm)."""
+    comms = ThreadComm.create(2)
+    real = ThreadComm.peer_addresses
+
+    def flaky(self, t, keep):
+        if self.rank == 1:
+            raise SeesawKernelError("simulated ssb_ipc_open failure")
+        return real(self, t, keep)
+
+    def body(r):
+        dev = torch.device("cuda", 0)
+        s = torch.cuda.Stream(dev)
+        with torch.cuda.stream(s):
+            comms[r].peer_addresses = flaky.__get__(comms[r])
+            ar = PeerArena(comms[r], dev, 256, 8, max_blocks=16)  # warns (RuntimeWarning) on both ranks
+            return ar.usable
+
+    assert run_threads(2, body) == [False, False]
