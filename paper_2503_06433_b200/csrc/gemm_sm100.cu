@@ -1128,7 +1128,7 @@ const Plan* measured_plan(int M, int N, int K, int epi) {
   return nullptr;
 }
 
-// SSB_GEMM_PLAN="M,N,K=mode:bn:splits;..." overrides the plan of exact
+// SSB_GEMM_PLAN="M,N,K=mode:bn:splits[:sk|:t];..." overrides the plan of exact
 // shapes (in-situ plan sweeps, tools/sweep_decode_plans.sh).
 bool env_plan(int M, int N, int K, Plan& out) {
   static const char* spec = getenv("SSB_GEMM_PLAN");
@@ -1136,11 +1136,20 @@ bool env_plan(int M, int N, int K, Plan& out) {
   for (const char* q = spec; *q;) {
     int m, n, k, mode, bn, sp, used = 0;
     if (sscanf(q, "%d,%d,%d=%d:%d:%d%n", &m, &n, &k, &mode, &bn, &sp, &used) != 6) return false;
+    q += used;
+    // optional suffix ":sk" (stream-K) or ":t" (split only the tail wave)
+    int sk = 0, tail = 0;
+    if (q[0] == ':' && q[1] == 's' && q[2] == 'k') {
+      sk = 1;
+      q += 3;
+    } else if (q[0] == ':' && q[1] == 't') {
+      tail = 1;
+      q += 2;
+    }
     if (m == M && n == N && k == K) {
-      out = Plan{mode, bn, sp, 0, 0};
+      out = Plan{mode, bn, sk ? 1 : sp, tail, sk};
       return true;
     }
-    q += used;
     while (*q == ';' || *q == ' ') ++q;
   }
   return false;
@@ -1150,7 +1159,7 @@ Plan choose_plan(int M, int N, int K, int epi, int sms, size_t ws_bytes) {
   Plan best{0, 256, 1};
   {
     Plan e;
-    if (env_plan(M, N, K, e) && (e.splits <= 1 || plan_ws_bytes(M, N, e, sms) <= ws_bytes)) return e;
+    if (env_plan(M, N, K, e) && ((e.splits <= 1 && !e.sk) || plan_ws_bytes(M, N, e, sms) <= ws_bytes)) return e;
   }
   double best_t = 1e30;
   const int bns[4] = {256, 224, 192, 128};
