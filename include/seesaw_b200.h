@@ -61,6 +61,11 @@ int ssb_set_pdl(int on);
  * the buffer it maps is released.  (Mapping it under the exporter's device
  * instead would leave the local GPU without peer access to it.)
  * Boundary for the reference's ReshardPlan transfers, reshard.py:125-201. */
+/* Debug only: CTA 0 of the next prefill attention pair-kernel launches
+ * writes its per-role timeline (5 x 4096 u64: globaltimer << 24 | event << 16
+ * | item << 8 | key tile) into buf; null turns it off.  tools/attn_trace.py. */
+int ssb_debug_attn_trace(void* buf);
+
 int ssb_ipc_export(const void* ptr, void* handle_out /* 64 bytes */, int64_t* offset_out);
 int ssb_ipc_open(const void* handle, int device, void** out_ptr);
 int ssb_ipc_close(void* ptr, int device);

@@ -127,6 +127,9 @@ def load() -> ctypes.CDLL:
             lib.ssb_device_sm_count.restype = ctypes.c_int
             lib.ssb_set_pdl.restype = ctypes.c_int
             lib.ssb_set_pdl.argtypes = [_I]
+            if hasattr(lib, "ssb_debug_attn_trace"):  # absent from older A/B builds (SSB_LIB)
+                lib.ssb_debug_attn_trace.restype = ctypes.c_int
+                lib.ssb_debug_attn_trace.argtypes = [_P]
             lib.ssb_ipc_export.restype = ctypes.c_int
             lib.ssb_ipc_export.argtypes = [_P, _P, ctypes.POINTER(ctypes.c_int64)]
             lib.ssb_ipc_open.restype = ctypes.c_int

@@ -730,6 +730,19 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, u
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate ? 1 : 0));
 }
 
+// Timeline trace of CTA 0 (debug only: ssb_debug_attn_trace sets the buffer;
+// null in production, one uniform branch per event).  Entry = globaltimer ns
+// << 24 | event << 16 | item round << 8 | key tile; role r owns
+// [r * kTraceCap, (r + 1) * kTraceCap).
+constexpr int kTraceCap = 4096;
+__device__ __forceinline__ void trace_ev(unsigned long long* tr, int role, int& n, int ev, int rnd, int j) {
+  if (tr == nullptr || blockIdx.x != 0 || n >= kTraceCap) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  tr[role * kTraceCap + n++] = (t << 24) | (static_cast<unsigned long long>(ev & 0xFF) << 16) |
+                               (static_cast<unsigned long long>(rnd & 0xFF) << 8) | (j & 0xFF);
+}
+
 struct PairIter {
   int first, rnd;
   int stride, n_items, n_qt_max, pairs, nseq;  // pairs = nq / 2
@@ -771,7 +784,9 @@ struct PairIter {
 template <int kPolyMask>
 __global__ void __launch_bounds__(kThreadsPair, 1)
     prefill_attn_tc_pair(const __grid_constant__ CUtensorMap tmap, const int32_t* __restrict__ cu, int nseq,
-                         int n_qt_max, int nq, int nk, __nv_bfloat16* __restrict__ out, int ldo, float scale_log2) {
+                         int n_qt_max, int nq, int nk, __nv_bfloat16* __restrict__ out, int ldo, float scale_log2,
+                         unsigned long long* __restrict__ trace, int st32) {
+  int ntr = 0;  // this thread's trace entries
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemPair::kBar);
@@ -836,6 +851,7 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
         const int n_kv = it.qt + 1;
         if (lane == 0) {
           mbar_wait(q_empty, (ic & 1) ^ 1);
+          trace_ev(trace, 0, ntr, 1, ic, 0);  // Q issue
           mbar_arrive_expect_tx(q_full, 2 * kTile);
           for (int hh = 0; hh < 2; ++hh)
             for (int sb = 0; sb < 2; ++sb)
@@ -850,6 +866,7 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
         for (int j = 0; j < n_kv; ++j, ++t) {
           const int st = t % depth;
           mbar_wait(&empty[st], ((t / depth) & 1) ^ 1);
+          trace_ev(trace, lane, ntr, 2, ic, j);  // K (lane 0) / V (lane 1) issue
           mbar_arrive_expect_tx(&full[st], kTile);
           for (int sb = 0; sb < 2; ++sb)
             tma_load_2d(smem + base + st * kTile + sb * kSub, &tmap, &full[st], col + sb * 64, it.start + j * kT,
@@ -868,6 +885,7 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
         // P(tt) of head hh (over its S columns) . V(tt) -> O
         if (first) mbar_wait(&o_free[hh], (ic & 1) ^ 1);  // the previous item's epilogue read O
         mbar_wait(&p_full[hh], tt & 1);
+        trace_ev(trace, 2, ntr, 10 + hh, ic, tt);  // PV issue (after P ready)
         tc_fence_after();
         const uint32_t v_base = smem_u32(smem + SmemPair::kV + (tt % kPairVSt) * kTile);
 #pragma unroll
@@ -879,11 +897,13 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
       while (it.next()) {
         const int n_kv = it.qt + 1;
         mbar_wait(q_full, ic & 1);
+        trace_ev(trace, 2, ntr, 3, ic, 0);  // Q landed
         tc_fence_after();
         const uint32_t q_base = smem_u32(smem + SmemPair::kQ);
         for (int j = 0; j < n_kv; ++j, ++t) {
           const int kst = t % kPairKSt;
           mbar_wait(&k_full[kst], (t / kPairKSt) & 1);
+          trace_ev(trace, 2, ntr, 4, ic, j);  // K landed
           if (j >= 1) mbar_wait(&v_full[(t - 1) % kPairVSt], ((t - 1) / kPairVSt) & 1);
           tc_fence_after();
           const uint32_t k_base = smem_u32(smem + SmemPair::kK + kst * kTile);
@@ -932,7 +952,9 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < n_kv; ++j, ++t) {
         // S(t) ready; pipe order also means every earlier P.V of this head is done (O stable)
+        if (r == 0) trace_ev(trace, 3 + hh, ntr, 20, ic, j);  // softmax waits for S
         mbar_wait(&s_full[hh], t & 1);
+        if (r == 0) trace_ev(trace, 3 + hh, ntr, 21, ic, j);  // S ready
         tc_fence_after();
         // raw scores: all four 32-column loads in flight, one wait.  With two
         // softmax warps per SMSP nothing hides a dependent chain, so the row
@@ -1003,9 +1025,11 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[hh]);
+        if (r == 0) trace_ev(trace, 3 + hh, ntr, 22, ic, j);  // P written
       }
       // epilogue: O / l of this head, then hand O back to the MMA warp
       mbar_wait(&o_done[hh], ic & 1);
+      if (r == 0) trace_ev(trace, 3 + hh, ntr, 23, ic, 0);  // O final
       tc_fence_after();
       const float inv = l > 0.f ? __frcp_rn(l) : 0.f;
       __nv_bfloat16* orow = out + static_cast<size_t>(start + qrow) * ldo + (2 * pair + hh) * kD;
@@ -1016,21 +1040,37 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
         for (int c = 0; c < kD / 32; ++c) tmem_ld32(o_acc + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + c * 32));
         tmem_ld_wait();
         if (qrow < len) {
-          uint4* dst = reinterpret_cast<uint4*>(orow);
+          // 32-byte stores (STG.256): each thread writes its own row, so every
+          // store instruction touches 32 rows -- half the L1 store wavefronts
+          // of 16-byte stores (the trace put this epilogue at ~1.5 us per item)
+          if (!st32) {
+            uint4* dst = reinterpret_cast<uint4*>(orow);
 #pragma unroll
-          for (int q = 0; q < kD / 8; ++q) {
-            uint4 o;
-            o.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]) * inv, __uint_as_float(v[8 * q + 1]) * inv);
-            o.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv);
-            o.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv);
-            o.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv);
-            dst[q] = o;
+            for (int q = 0; q < kD / 8; ++q) {
+              uint4 o;
+              o.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]) * inv, __uint_as_float(v[8 * q + 1]) * inv);
+              o.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv);
+              o.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv);
+              o.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv);
+              dst[q] = o;
+            }
+          } else
+#pragma unroll
+          for (int q = 0; q < kD / 16; ++q) {
+            uint32_t o[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              o[k] = pack_bf16x2(__uint_as_float(v[16 * q + 2 * k]) * inv, __uint_as_float(v[16 * q + 2 * k + 1]) * inv);
+            asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(orow + 16 * q), "r"(o[0]), "r"(o[1]),
+                         "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7])
+                         : "memory");
           }
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_free[hh]);
+      if (r == 0) trace_ev(trace, 3 + hh, ntr, 24, ic, 0);  // epilogue done
       ++ic;
     }
   }
@@ -1043,6 +1083,8 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
 }
 
 }  // namespace
+
+unsigned long long* g_attn_trace = nullptr;  // ssb_debug_attn_trace
 
 int launch_prefill_attn_tc(const void* qkv, int ld, int T, int nq, int nk, const int32_t* cu, int nseq,
                            int max_len, void* out, int ldo, float scale, cudaStream_t s, bool persistent) {
@@ -1069,7 +1111,8 @@ int launch_prefill_attn_tc(const void* qkv, int ld, int T, int nq, int nk, const
     const long items = static_cast<long>(n_qt) * (nq / 2) * nseq;
     const int grid = static_cast<int>(std::min<long>(num_sms(), items));
     kern<<<grid, kThreadsPair, SmemPair::kBytes, s>>>(map, cu, nseq, n_qt, nq, nk, static_cast<__nv_bfloat16*>(out),
-                                                     ldo, scale * 1.4426950408889634f);
+                                                     ldo, scale * 1.4426950408889634f, g_attn_trace,
+                                                     (reinterpret_cast<uintptr_t>(out) % 32 == 0 && ldo % 16 == 0) ? 1 : 0);
     return check_launch("prefill_attn_tc_pair");
   }
   if (persistent) {
@@ -1098,3 +1141,11 @@ int launch_prefill_attn_tc(const void* qkv, int ld, int T, int nq, int nk, const
 }
 
 }  // namespace ssb
+
+// Debug only: record CTA 0's timeline of the next prefill_attn_tc_pair
+// launches into buf (5 roles x 4096 u64 entries, zeroed by the caller); null
+// turns it off.
+extern "C" int ssb_debug_attn_trace(void* buf) {
+  ssb::g_attn_trace = static_cast<unsigned long long*>(buf);
+  return 0;
+}

@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
 def test_ctypes_signatures_cover_header():
     declared = set(declared_functions())
     bound = set(_lib.SIGNATURES) | {"ssb_last_error", "ssb_version", "ssb_device_sm_count", "ssb_gemm_plan",
-                                    "ssb_tp_signal_bytes", "ssb_set_pdl", "ssb_ipc_export", "ssb_ipc_open",
+                                    "ssb_tp_signal_bytes", "ssb_set_pdl", "ssb_ipc_export", "ssb_ipc_open", "ssb_debug_attn_trace",
                                     "ssb_ipc_close"}
     assert declared == bound
 
