@@ -195,9 +195,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(&s_free[st]);
       const int k0 = j * kT;
       if (j == n_kv - 1 || k0 + kT > len) {
+        const int lim = min(qrow + 1, len) - k0;
 #pragma unroll
-        for (int i = 0; i < kT; ++i)
-          if (k0 + i > qrow || k0 + i >= len) s[i] = -INFINITY;
+        for (int i = 0; i < kT; ++i) s[i] = i < lim ? s[i] : -INFINITY;
       }
       float mx = -INFINITY;
 #pragma unroll
@@ -557,9 +557,10 @@ __global__ void __launch_bounds__(kThreadsP, 1)
         if (lane == 0) mbar_arrive(&s_free[ss]);
         const int k0 = j * kT + c0;
         if (j == qt || j * kT + kT > len) {
+          // valid keys of this row in the tile: one compare + select per key
+          const int lim = min(qrow + 1, len) - k0;
 #pragma unroll
-          for (int i = 0; i < kT / 2; ++i)
-            if (k0 + i > qrow || k0 + i >= len) s[i] = -INFINITY;
+          for (int i = 0; i < kT / 2; ++i) s[i] = i < lim ? s[i] : -INFINITY;
         }
         float mx = -INFINITY;
 #pragma unroll
@@ -710,6 +711,29 @@ __device__ __forceinline__ float exp2_poly(float x) {
   const float f = x - (t - 12582912.f);
   const float p = fmaf(fmaf(fmaf(0.05502927f, f, 0.24225698f), f, 0.69325305f), f, 0.99995134f);
   return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
+
+// Packed fp32x2 arithmetic (Blackwell FFMA2 / FADD2): two lanes per
+// instruction, each lane rounded exactly like fmaf / + (bit-identical).
+__device__ __forceinline__ float2 ffma2_bcast(float x0, float x1, float s, float c) {
+  unsigned long long x, r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(x0), "f"(x1));
+  asm("{\n\t.reg .b64 sc, cc;\n\tmov.b64 sc, {%2, %2};\n\tmov.b64 cc, {%3, %3};\n\t"
+      "fma.rn.f32x2 %0, %1, sc, cc;\n\t}"
+      : "=l"(r)
+      : "l"(x), "f"(s), "f"(c));
+  float2 o;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+  return o;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long x, y, r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(y) : "f"(b.x), "f"(b.y));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+  float2 o;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+  return o;
 }
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
@@ -971,9 +995,12 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
         }
         const int k0 = j * kT;
         if (j == qt || k0 + kT > len) {
+          // valid keys of this row in the tile: one compare + select per key
+          // (was two compares, an add and a select: the diagonal tile's mask
+          // cost more instructions than the rest of its softmax)
+          const int lim = min(qrow + 1, len) - k0;
 #pragma unroll
-          for (int i = 0; i < kT; ++i)
-            if (k0 + i > qrow || k0 + i >= len) sv[i] = -INFINITY;
+          for (int i = 0; i < kT; ++i) sv[i] = i < lim ? sv[i] : -INFINITY;
         }
         float m8[8];
 #pragma unroll
@@ -1000,9 +1027,12 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
             tmem_st32(o_acc + c * 32, v);
           }
         }
-        float s8[8];
+        // row sum on 4 packed accumulator pairs (s8[2k], s8[2k+1]) -- the
+        // same 8 partial sums in the same order as scalar code, half the
+        // instructions; the exponent argument s * c - m likewise as FFMA2
+        float2 s4[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) s8[i] = 0.f;
+        for (int i = 0; i < 4; ++i) s4[i] = make_float2(0.f, 0.f);
         const float nm = -m_used;
         // P over the first 64 columns of this head's S accumulator, 32 keys at a time
 #pragma unroll
@@ -1010,17 +1040,16 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float a = fast_exp2(fmaf(sv[c * 32 + 2 * i], scale_log2, nm));
-            const float xb = fmaf(sv[c * 32 + 2 * i + 1], scale_log2, nm);
-            const float b = (i & kPolyMask) ? exp2_poly(xb) : fast_exp2(xb);
-            s8[(2 * i) & 7] += a;
-            s8[(2 * i + 1) & 7] += b;
+            const float2 x = ffma2_bcast(sv[c * 32 + 2 * i], sv[c * 32 + 2 * i + 1], scale_log2, nm);
+            const float a = fast_exp2(x.x);
+            const float b = (i & kPolyMask) ? exp2_poly(x.y) : fast_exp2(x.y);
+            s4[i & 3] = fadd2(s4[i & 3], make_float2(a, b));
             pk[i] = pack_bf16x2(a, b);
           }
           tmem_st16(s_acc + c * 16, pk);
         }
         tmem_st_wait();
-        const float sum = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
+        const float sum = ((s4[0].x + s4[0].y) + (s4[1].x + s4[1].y)) + ((s4[2].x + s4[2].y) + (s4[3].x + s4[3].y));
         l = l * corr + sum;
         tc_fence_before();
         __syncwarp();
