@@ -726,6 +726,14 @@ __device__ __forceinline__ float2 ffma2_bcast(float x0, float x1, float s, float
   asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
   return o;
 }
+__device__ __forceinline__ float2 fmul2_bcast(float x0, float x1, float s) {
+  unsigned long long x, r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(x0), "f"(x1));
+  asm("{\n\t.reg .b64 sc;\n\tmov.b64 sc, {%2, %2};\n\tmul.rn.f32x2 %0, %1, sc;\n\t}" : "=l"(r) : "l"(x), "f"(s));
+  float2 o;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+  return o;
+}
 __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   unsigned long long x, y, r;
   asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a.x), "f"(a.y));
@@ -1088,8 +1096,10 @@ __global__ void __launch_bounds__(kThreadsPair, 1)
           for (int q = 0; q < kD / 16; ++q) {
             uint32_t o[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-              o[k] = pack_bf16x2(__uint_as_float(v[16 * q + 2 * k]) * inv, __uint_as_float(v[16 * q + 2 * k + 1]) * inv);
+            for (int k = 0; k < 8; ++k) {
+              const float2 y = fmul2_bcast(__uint_as_float(v[16 * q + 2 * k]), __uint_as_float(v[16 * q + 2 * k + 1]), inv);
+              o[k] = pack_bf16x2(y.x, y.y);
+            }
             asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(orow + 16 * q), "r"(o[0]), "r"(o[1]),
                          "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7])
                          : "memory");
