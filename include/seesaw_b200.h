@@ -65,6 +65,10 @@ int ssb_set_pdl(int on);
  * writes its per-role timeline (5 x 4096 u64: globaltimer << 24 | event << 16
  * | item << 8 | key tile) into buf; null turns it off.  tools/attn_trace.py. */
 int ssb_debug_attn_trace(void* buf);
+/* Debug only: stream `bytes` from src through shared memory with bulk copies
+ * (ctas_per_sm x #SMs CTAs, chunk-byte pieces, a stages-deep ring), reading
+ * nothing back -- the HBM read ceiling for a TMA-fed kernel. */
+int ssb_debug_read_stream(const void* src, int64_t bytes, int ctas_per_sm, int chunk, int stages, void* stream);
 
 int ssb_ipc_export(const void* ptr, void* handle_out /* 64 bytes */, int64_t* offset_out);
 int ssb_ipc_open(const void* handle, int device, void** out_ptr);

@@ -102,6 +102,7 @@ SIGNATURES: dict[str, list] = {
     "ssb_tp_allreduce_rmsnorm": [_PU64, _PU64, _PU64, _PU64, _I, _I, _I, _I, _I, _P, _F, ctypes.c_uint32, _I, _P,
                                  _P],
     "ssb_tp_allreduce_rowss": [_PU64, _PU64, _PU64, _PU64, _I, _I, _I, _I, _I, ctypes.c_uint32, _I, _P, _P],
+    "ssb_debug_read_stream": [_P, _I64, _I, _I, _I, _P],
     "ssb_tp_argmax_keys": [_PU64, _PU64, _I, _I, _I, _P, ctypes.c_uint32, _I, _P, _P],
 }
 
@@ -141,6 +142,8 @@ def load() -> ctypes.CDLL:
             lib.ssb_tp_signal_bytes.restype = ctypes.c_size_t
             lib.ssb_tp_signal_bytes.argtypes = []
             for name, args in SIGNATURES.items():
+                if name.startswith("ssb_debug_") and not hasattr(lib, name):
+                    continue  # older A/B builds (SSB_LIB) lack the debug entry points
                 fn = getattr(lib, name)
                 fn.argtypes = args
                 fn.restype = ctypes.c_int

@@ -660,6 +660,232 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// Warp-specialised variant (default): a 5th warp is the TMA producer, and
+// every consumer warp copies its K and V fragments of a block from the ring
+// into registers (ldmatrix) and releases the slot BEFORE its MMAs and
+// softmax, so a slot is refilled as soon as the four warps have read it --
+// not after the slowest warp finished computing on it (thread 0 used to wait
+// for that before issuing the refill).  The ring's bytes in flight then
+// stay close to its size: the kernel was at ~6.6 TB/s while a bare
+// bulk-copy read stream with the same 192 KB in flight per SM reads
+// 7.3 TB/s on the same box (tools/read_bw.py).
+template <int D, int kPStages>
+__global__ void __launch_bounds__(160)
+    decode_attn_persistent_ws(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* __restrict__ qkv,
+                           int ld, int nq, int nk, const int32_t* __restrict__ block_tables, int max_blocks,
+                           const int32_t* __restrict__ ctx_lens, int B, ssb_kv_geometry geo, int layer,
+                           __nv_bfloat16* __restrict__ out, int ldo, float scale_log2) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  using S = DecodeSmemP<D, kPStages>;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kRing);
+  uint64_t* empty = full + kPStages;
+  float* sm_m = reinterpret_cast<float*>(smem + S::kRing + 64);  // [4][16]
+  float* sm_l = sm_m + 4 * 16;                                   // [4][16]
+  float* sm_o = sm_l + 4 * 16;                                   // [4][G][D]
+  const int G = nq / nk;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_items = B * nk;
+  griddep_launch_dependents();
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tmap);
+    for (int st = 0; st < kPStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 4);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // ---- producer (warp 4, lane 0): next (item, block) to load ----
+  int p_item = blockIdx.x, p_blk = 0, p_nblk = 0;
+  uint32_t p_count = 0;  // blocks issued so far (ring slot = p_count % kPStages)
+  auto p_seek = [&]() {  // skip to an item with blocks left
+    while (p_item < n_items) {
+      if (p_blk == 0) p_nblk = (ctx_lens[p_item / nk] + kBlk - 1) / kBlk;
+      if (p_blk < p_nblk) return true;
+      p_item += gridDim.x;
+      p_blk = 0;
+    }
+    return false;
+  };
+  auto issue_next = [&]() {
+    if (!p_seek()) return;
+    const int st = p_count % kPStages;
+    const int b = p_item / nk, kvh = p_item - (p_item / nk) * nk;
+    const int64_t blk = block_tables[static_cast<size_t>(b) * max_blocks + p_blk];
+    const int row_k = static_cast<int>((((blk * geo.n_layers + layer) * 2 + 0) * geo.n_heads + kvh) * kBlk);
+    const int row_v = static_cast<int>((((blk * geo.n_layers + layer) * 2 + 1) * geo.n_heads + kvh) * kBlk);
+    uint8_t* kt = smem + st * S::kStage;
+    uint8_t* vt = kt + S::kTile;
+    mbar_arrive_expect_tx(&full[st], S::kStage);
+#pragma unroll
+    for (int sub = 0; sub < D / 64; ++sub) {
+      tma_load_2d(kt + sub * kBlk * 128, &tmap, &full[st], sub * 64, row_k, policy_evict_first());
+      tma_load_2d(vt + sub * kBlk * 128, &tmap, &full[st], sub * 64, row_v, policy_evict_first());
+    }
+    ++p_count;
+    ++p_blk;
+  };
+  // PDL: this kernel may start while the QKV GEMM that appends the current
+  // token's K/V (and writes Q) still runs.  Every pool block but a sequence's
+  // LAST one holds only older tokens, so those may stream into the ring now;
+  // Q and the last blocks are read only after griddep_wait().
+  if (warp == 4) {
+    if (lane == 0) {
+      while (p_count < kPStages && p_seek() && p_blk + 1 < p_nblk) issue_next();
+      griddep_wait();
+      while (p_seek()) {
+        // slot of block p_count: free once block p_count - kPStages was read
+        if (p_count >= kPStages) mbar_wait(&empty[p_count % kPStages], ((p_count / kPStages) & 1) ^ 1);
+        issue_next();
+      }
+    }
+    return;
+  }
+  griddep_wait();  // consumers read Q (written by the predecessor)
+
+  uint32_t c_count = 0;  // blocks consumed so far
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int b = item / nk, kvh = item - (item / nk) * nk;
+    const int ctx = ctx_lens[b];
+    const int nblk = (ctx + kBlk - 1) / kBlk;
+    uint32_t qf[D / 16][4];
+    {
+      const int r0 = lane >> 2, r1 = r0 + 8;
+      const __nv_bfloat16* q = qkv + static_cast<size_t>(b) * ld + static_cast<size_t>(kvh) * G * D;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const int c = kk * 16 + (lane & 3) * 2;
+        qf[kk][0] = r0 < G ? *reinterpret_cast<const uint32_t*>(q + r0 * D + c) : 0u;
+        qf[kk][1] = r1 < G ? *reinterpret_cast<const uint32_t*>(q + r1 * D + c) : 0u;
+        qf[kk][2] = r0 < G ? *reinterpret_cast<const uint32_t*>(q + r0 * D + c + 8) : 0u;
+        qf[kk][3] = r1 < G ? *reinterpret_cast<const uint32_t*>(q + r1 * D + c + 8) : 0u;
+      }
+    }
+    float o[D / 8][4];
+#pragma unroll
+    for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
+
+    for (int j = 0; j < nblk; ++j, ++c_count) {
+      const int st = c_count % kPStages;
+      const uint32_t parity = (c_count / kPStages) & 1;
+      mbar_wait(&full[st], parity);
+      const uint32_t kt = smem_u32(smem + st * S::kStage);
+      const uint32_t vt = kt + S::kTile;
+      // this warp's 16 tokens of K and V into registers, then release the slot
+      uint32_t kf[D / 16][4], vf[D / 16][4];
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const int n = warp * 16 + (lane & 7) + ((lane >> 4) << 3);
+        const int k = kk * 16 + ((lane >> 3) & 1) * 8;
+        ldsm_x4(kt + swz(n, k, kBlk), kf[kk][0], kf[kk][1], kf[kk][2], kf[kk][3]);
+      }
+#pragma unroll
+      for (int dp = 0; dp < D / 16; ++dp) {
+        const int t = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        const int c = dp * 16 + (lane >> 4) * 8;
+        ldsm_x4_t(vt + swz(t, c, kBlk), vf[dp][0], vf[dp][1], vf[dp][2], vf[dp][3]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      float sc[2][4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) sc[i][0] = sc[i][1] = sc[i][2] = sc[i][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        mma16816(sc[0], qf[kk], kf[kk][0], kf[kk][1]);
+        mma16816(sc[1], qf[kk], kf[kk][2], kf[kk][3]);
+      }
+      const int kv0 = j * kBlk + warp * 16;
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int kv = kv0 + i * 8 + (lane & 3) * 2 + (e & 1);
+          sc[i][e] = kv < ctx ? sc[i][e] * scale_log2 : -INFINITY;
+        }
+      float corr[2];
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+        float mx = fmaxf(fmaxf(sc[0][2 * hr], sc[0][2 * hr + 1]), fmaxf(sc[1][2 * hr], sc[1][2 * hr + 1]));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float m_new = fmaxf(m_r[hr], mx);
+        const float m_use = m_new == -INFINITY ? 0.f : m_new;
+        corr[hr] = exp2f(m_r[hr] - m_use);
+        m_r[hr] = m_new;
+        float sum = 0.f;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          sc[i][2 * hr] = exp2f(sc[i][2 * hr] - m_use);
+          sc[i][2 * hr + 1] = exp2f(sc[i][2 * hr + 1] - m_use);
+          sum += sc[i][2 * hr] + sc[i][2 * hr + 1];
+        }
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        l_r[hr] = l_r[hr] * corr[hr] + sum;
+      }
+#pragma unroll
+      for (int i = 0; i < D / 8; ++i) {
+        o[i][0] *= corr[0];
+        o[i][1] *= corr[0];
+        o[i][2] *= corr[1];
+        o[i][3] *= corr[1];
+      }
+      uint32_t a[4];
+      a[0] = pack_bf16x2(sc[0][0], sc[0][1]);
+      a[1] = pack_bf16x2(sc[0][2], sc[0][3]);
+      a[2] = pack_bf16x2(sc[1][0], sc[1][1]);
+      a[3] = pack_bf16x2(sc[1][2], sc[1][3]);
+#pragma unroll
+      for (int dp = 0; dp < D / 16; ++dp) {
+        mma16816(o[2 * dp], a, vf[dp][0], vf[dp][1]);
+        mma16816(o[2 * dp + 1], a, vf[dp][2], vf[dp][3]);
+      }
+    }
+    // merge the 4 warps' partial states (rows < G are real) in the merge region
+    const int r0 = lane >> 2, r1 = r0 + 8;
+    if ((lane & 3) == 0) {
+      sm_m[warp * 16 + r0] = m_r[0];
+      sm_m[warp * 16 + r1] = m_r[1];
+      sm_l[warp * 16 + r0] = l_r[0];
+      sm_l[warp * 16 + r1] = l_r[1];
+    }
+#pragma unroll
+    for (int i = 0; i < D / 8; ++i) {
+      const int c = i * 8 + (lane & 3) * 2;
+      if (r0 < G) {
+        sm_o[(warp * G + r0) * D + c] = o[i][0];
+        sm_o[(warp * G + r0) * D + c + 1] = o[i][1];
+      }
+      if (r1 < G) {
+        sm_o[(warp * G + r1) * D + c] = o[i][2];
+        sm_o[(warp * G + r1) * D + c + 1] = o[i][3];
+      }
+    }
+    named_bar_sync(1, 128);
+    for (int idx = threadIdx.x; idx < G * D; idx += 128) {
+      const int r = idx / D, c = idx - r * D;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) M = fmaxf(M, sm_m[w * 16 + r]);
+      const float Mu = M == -INFINITY ? 0.f : M;
+      float L = 0.f, acc = 0.f;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const float f = exp2f(sm_m[w * 16 + r] - Mu);
+        L += sm_l[w * 16 + r] * f;
+        acc += sm_o[(w * G + r) * D + c] * f;
+      }
+      out[static_cast<size_t>(b) * ldo + (kvh * G + r) * D + c] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
+    }
+    named_bar_sync(1, 128);  // the merge region is rewritten by the next item
+  }
+}
+
 template <int D>
 int launch_prefill(const void* qkv, int ld, int nq, int nk, const int32_t* cu, int nseq, int max_len,
                    void* out, int ldo, float scale, cudaStream_t s) {
@@ -679,23 +905,25 @@ int launch_prefill(const void* qkv, int ld, int nq, int nk, const int32_t* cu, i
 template <int D, int ST>
 int launch_decode_p(const CUtensorMap& map, const void* qkv, int ld, int nq, int nk, ssb_kv_geometry geo, int layer,
                     const int32_t* tables, int max_blocks, const int32_t* ctx, int B, void* out, int ldo, float scale,
-                    int ctas_per_sm, cudaStream_t s) {
+                    int ctas_per_sm, cudaStream_t s, bool ws) {
   const int G = nq / nk;
   const int smem = DecodeSmemP<D, ST>::bytes(G);
-  static int attr_p = 0;
-  if (attr_p < smem) {
-    SSB_CUDA(cudaFuncSetAttribute(decode_attn_persistent<D, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr_p = smem;
+  auto kern = ws ? decode_attn_persistent_ws<D, ST> : decode_attn_persistent<D, ST>;
+  const int threads = ws ? 160 : 128;
+  static int attr_p[2] = {0, 0};
+  if (attr_p[ws] < smem) {
+    SSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_p[ws] = smem;
   }
   int per_sm = 0;
-  SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_attn_persistent<D, ST>, 128, smem));
+  SSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
   if (ctas_per_sm > 0) per_sm = std::min(per_sm, ctas_per_sm);
   const long items = static_cast<long>(B) * nk;
   const int grid = static_cast<int>(std::min<long>(items, static_cast<long>(std::max(per_sm, 1)) * num_sms()));
   const bool pdl = pdl_enabled();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(128);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -703,10 +931,9 @@ int launch_decode_p(const CUtensorMap& map, const void* qkv, int ld, int nq, int
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  SSB_CUDA(cudaLaunchKernelEx(&cfg, decode_attn_persistent<D, ST>, map, static_cast<const __nv_bfloat16*>(qkv), ld, nq,
-                              nk, tables, max_blocks, ctx, B, geo, layer, static_cast<__nv_bfloat16*>(out), ldo,
-                              scale * kLog2e));
-  return check_launch("decode_attn_persistent");
+  SSB_CUDA(cudaLaunchKernelEx(&cfg, kern, map, static_cast<const __nv_bfloat16*>(qkv), ld, nq, nk, tables, max_blocks,
+                              ctx, B, geo, layer, static_cast<__nv_bfloat16*>(out), ldo, scale * kLog2e));
+  return check_launch(ws ? "decode_attn_persistent_ws" : "decode_attn_persistent");
 }
 
 template <int D>
@@ -723,24 +950,31 @@ int launch_decode(const void* qkv, int ld, int nq, int nk, const void* pool, ssb
   int rc = encode_tmap_2d_bf16(&map, pool, D, rows, D * 2, 64, 64);
   if (rc) return rc;
   static const int variant = [] {
-    const char* e = getenv("SSB_DECODE_ATTN_VARIANT");  // A/B: 1 = one CTA per (sequence, KV head)
+    // A/B: 1 = one CTA per (sequence, KV head); 2 = persistent with the
+    // refill issued by consumer thread 0 (before the producer warp)
+    const char* e = getenv("SSB_DECODE_ATTN_VARIANT");
     return e ? atoi(e) : 0;
   }();
-  if (variant == 0) {
+  if (variant == 0 || variant == 2) {
+    const bool ws = variant == 0;
     // ring depth x CTAs per SM (SSB_DECODE_STAGES, SSB_DECODE_CTAS: A/B knobs)
-    static const int stages = [] {
+    // measured in the decode step (profiles/r02/decode_attn_ws_sweep.jsonl):
+    // the producer-warp kernel is fastest with a 2-deep ring (2 CTAs per SM,
+    // register-limited) -- 18.43 vs 18.72 ms per 8B decode step for the
+    // thread-0-refill kernel at its best (3 stages)
+    static const int stages = [ws] {
       const char* e = getenv("SSB_DECODE_STAGES");
-      return e ? atoi(e) : 3;
+      return e ? atoi(e) : (ws ? 2 : 3);
     }();
     static const int ctas = [] {
       const char* e = getenv("SSB_DECODE_CTAS");
       return e ? atoi(e) : 0;
     }();
     switch (stages) {
-      case 2: return launch_decode_p<D, 2>(map, qkv, ld, nq, nk, geo, layer, tables, max_blocks, ctx, B, out, ldo, scale, ctas, s);
-      case 4: return launch_decode_p<D, 4>(map, qkv, ld, nq, nk, geo, layer, tables, max_blocks, ctx, B, out, ldo, scale, ctas, s);
-      case 6: return launch_decode_p<D, 6>(map, qkv, ld, nq, nk, geo, layer, tables, max_blocks, ctx, B, out, ldo, scale, ctas, s);
-      default: return launch_decode_p<D, 3>(map, qkv, ld, nq, nk, geo, layer, tables, max_blocks, ctx, B, out, ldo, scale, ctas, s);
+      case 2: return launch_decode_p<D, 2>(map, qkv, ld, nq, nk, geo, layer, tables, max_blocks, ctx, B, out, ldo, scale, ctas, s, ws);
+      case 4: return launch_decode_p<D, 4>(map, qkv, ld, nq, nk, geo, layer, tables, max_blocks, ctx, B, out, ldo, scale, ctas, s, ws);
+      case 6: return launch_decode_p<D, 6>(map, qkv, ld, nq, nk, geo, layer, tables, max_blocks, ctx, B, out, ldo, scale, ctas, s, ws);
+      default: return launch_decode_p<D, 3>(map, qkv, ld, nq, nk, geo, layer, tables, max_blocks, ctx, B, out, ldo, scale, ctas, s, ws);
     }
   }
   static bool attr = false;

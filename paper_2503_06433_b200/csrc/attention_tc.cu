@@ -310,9 +310,6 @@ struct SmemP {
 };
 constexpr int kThreadsP = 320;  // TMA warp, MMA warp, 8 softmax warps (two per TMEM lane quadrant)
 
-__device__ __forceinline__ void named_bar_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 
 
 // Item of round r for CTA `first` of `stride` CTAs: boustrophedon order (odd

@@ -199,6 +199,11 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
   return r;
 }
 
+// Barrier over the first n threads' warps that use id (a subset of the CTA).
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
