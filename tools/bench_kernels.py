@@ -168,3 +168,37 @@ def bench_decode_attn():
 
 if __name__ == "__main__" and "--what" in sys.argv and sys.argv[sys.argv.index("--what") + 1] == "decode":
     bench_decode_attn()
+
+
+def bench_l2_prefetch():
+    """Does an L2-resident weight make the M = 512 decode projections faster?
+    Each decode projection runs right after decode attention streamed ~2 GB of
+    KV through L2 (weights cold, from HBM).  Time o_proj / QKV / down after
+    (a) a 2 GiB streaming read (cold weights) and (b) the same read followed
+    by a pass over the weight (weights L2-resident), CUDA events on the GEMM."""
+    ws = torch.zeros(64 << 20, dtype=torch.uint8, device="cuda")
+    junk = torch.empty(1 << 30, dtype=torch.bfloat16, device="cuda").uniform_()
+    for M, N, K in ((512, 4096, 4096), (512, 6144, 4096), (512, 4096, 14336)):
+        a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        w = (torch.randn(N, K, device="cuda") / K**0.5).to(torch.bfloat16)
+        c = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        res = {}
+        for warm in (0, 1):
+            ts = []
+            for _ in range(15):
+                junk.sum()
+                if warm:
+                    w.view(torch.int32).amax()  # pulls w through L2
+                s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s_.record()
+                ops.gemm(a, w, out=c, workspace=ws)
+                e_.record()
+                e_.synchronize()
+                ts.append(s_.elapsed_time(e_))
+            ts.sort()
+            res["warm" if warm else "cold"] = ts[len(ts) // 2] * 1e3
+        print(json.dumps({"what": "l2_prefetch", "M": M, "N": N, "K": K, "us": res}), flush=True)
+
+
+if __name__ == "__main__" and "--what" in sys.argv and sys.argv[sys.argv.index("--what") + 1] == "l2pf":
+    bench_l2_prefetch()
