@@ -242,7 +242,7 @@ def run_ours(args) -> None:
                 "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "traffic_algorithmic_bytes": alg_bytes,
                 "traffic_source": "ncu --set full, DRAM read+write bytes per launch, mean of the 4 projections of "
-                                  "one prefill layer (profiles/r01/ncu_full_gemm_prefill.json)",
+                                  f"one prefill layer ({_gemm_prefill_traffic_file()})",
                 "all_gemm_tflops": kern.get("gemm", {}).get("tflops"),
                 "peak_source": f"{peaks['source']} bf16_tflops_sustained"}
     da = kern.get("decode_attention", {})
@@ -348,11 +348,19 @@ def allreduce_table(worker, dev, world: int, arch, rows: int = 512, iters: int =
     return out
 
 
+def _gemm_prefill_traffic_file() -> str:
+    for r in ("r02", "r01"):
+        if (ROOT / "profiles" / r / "ncu_full_gemm_prefill.json").exists():
+            return f"profiles/{r}/ncu_full_gemm_prefill.json"
+    return "none"
+
+
 def _gemm_prefill_traffic(arch, args):
     """(mean ncu DRAM bytes per launch, mean algorithmic bytes per launch) of
     the prefill projections.  The DRAM bytes come from the committed ncu
     capture of the bench command; algorithmic = A + B + C (+ residual)."""
-    p = ROOT / "profiles" / "r01" / "ncu_full_gemm_prefill.json"
+    p = next((q for q in (ROOT / "profiles" / r / "ncu_full_gemm_prefill.json" for r in ("r02", "r01")) if q.exists()),
+             ROOT / "profiles" / "r01" / "ncu_full_gemm_prefill.json")
     traffic = None
     if p.exists():
         rows = json.loads(p.read_text())
