@@ -238,7 +238,7 @@ class _IpcMapping:
     its last holder)."""
 
     _open: dict = {}
-    _lock = threading.Lock()
+    _lock = threading.RLock()  # re-entrant: a GC-triggered __del__ may run inside open()
 
     def __init__(self, key, base: int) -> None:
         self.key, self.base = key, base
