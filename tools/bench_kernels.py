@@ -145,7 +145,9 @@ if __name__ == "__main__" and "--what" in sys.argv and sys.argv[sys.argv.index("
 def bench_decode_attn():
     """Decode attention at the bench shape (8B: 512 sequences, ctx 1152,
     32/8 heads, 32-layer pool of 64-token blocks), algorithmic GB/s."""
-    B, nq, nk, d, BS, ctx = 512, 32, 8, 128, 64, 1152
+    ctx = int(os.environ.get("DEC_CTX", "1152"))
+    B = int(os.environ.get("DEC_B", str(512 * 1152 // ctx)))  # same KV bytes by default
+    nq, nk, d, BS = 32, 8, 128, 64
     L = int(os.environ.get("DEC_LAYERS", "32"))
     seq_tables = os.environ.get("DEC_SEQ", "0") == "1"
     nb = B * (ctx // BS + 2)
@@ -160,7 +162,7 @@ def bench_decode_attn():
     ms = timed(lambda: ops.decode_attention(qkv, nq, nk, pool, (L, nk, BS, d), nb, layer, tables, ctxs, out,
                                             d ** -0.5), iters=30, flush=False)
     gb = B * ctx * 2 * nk * d * 2 / 1e9
-    print(json.dumps({"what": "decode_attn", "ms": ms, "gbs": gb / ms * 1e3,
+    print(json.dumps({"what": "decode_attn", "ms": ms, "gbs": gb / ms * 1e3, "B": B, "ctx": ctx,
                       "stages": os.environ.get("SSB_DECODE_STAGES", "3"), "ctas": os.environ.get("SSB_DECODE_CTAS", "0"),
                       "variant": os.environ.get("SSB_DECODE_ATTN_VARIANT", "0"), "layers": L,
                       "sequential_blocks": seq_tables}), flush=True)
