@@ -277,6 +277,8 @@ def run_ours(args) -> None:
         "reference_model_prediction": _predict(model, hw, cfg_p, cfg_d, args),
         "clocks": clocks,
         "decode_attention_hbm_frac": (da.get("gbs", 0) / peaks["hbm_gbs"]) if da else None,
+        # prompt + output tokens per second beside the output-only metric
+        "prompt_plus_output_tokens_per_s": args.prompts * (args.input_len + args.output_len) / mean_t,
     }
     if ar_table is not None:
         line["allreduce_table"] = ar_table
